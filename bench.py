@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py — variant-steps/sec of the B200 batched-simulation hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model box] [--variants 16384] [--sim-steps 1000]
+
+A bench "step" is one pass of the hot path over one batch: every variant of
+the per-GPU batch simulated through all `--sim-steps` physics steps (one
+persistent-kernel launch).  Default workload = BASELINE.json configs[1]:
+box, 16 384 variants x 1 000 steps per GPU (weak scaling for N > 1: each rank
+gets a contiguous 16 384-seed slice of the global batch from the N-way
+splitter).
+
+value : device-resident inputs, CUDA events on the kernel's stream around
+        each launch, L2 flushed (256 MiB write) between launches outside the
+        event pair; max over ranks.
+e2e   : the drop-in call GpuExecutor.run -> hb_run_batch with HOST seeds:
+        host initialiser, H2D of the initial state, kernel, D2H of the
+        32-byte results, all inside the timed region (wall clock, max over ranks).
+--impl reference : the reference's own cpu_executor (oracle/_ref, compiled
+        from /root/reference/proj/src) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "variant-steps/sec (whole box) vs #variants & steps; speedup over host-CPU ref"
+MODELS = ("box", "box_and_ball", "arm_with_rope", "humanoid")
+# Algorithmic FP64 ops per variant-step (add/sub/mul/div/sqrt = 1,
+# compares excluded): 16n + 8m*(19 + sqrt + div).
+W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240}
+BODIES = {"box": 1, "box_and_ball": 2, "arm_with_rope": 12, "humanoid": 32}
+CONS = {"box": 0, "box_and_ball": 1, "arm_with_rope": 11, "humanoid": 46}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="box", choices=MODELS)
+    ap.add_argument("--variants", type=int, default=16384, help="variants per GPU")
+    ap.add_argument("--sim-steps", type=int, default=1000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(a):
+    tag = " (BASELINE configs[1])" if (a.model, a.variants, a.sim_steps) == ("box", 16384, 1000) else ""
+    return f"{a.model} {a.variants} variants x {a.sim_steps} steps per GPU{tag}"
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.th = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.th = threading.Thread(target=self._read, daemon=True)
+        self.th.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.th:
+            self.th.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------- helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_traffic(model, variants, sim_steps):
+    """dram bytes per launch from the committed ncu capture, if one matches."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(f"{model}/{variants}/{sim_steps}")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_reference_rate(model_idx, n, sim_steps, reps=3):
+    """Reference cpu_executor(workers = hardware_concurrency) on the host; best
+    of `reps` runs of a bounded sample (the full workload when it is small)."""
+    import oracle as O
+    if not O.ref_available():
+        return None
+    cores = O.ref_hardware_concurrency()
+    per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[model_idx]
+    est_s = n * sim_steps * per_vs_core_ns * 1e-9 / cores * reps
+    # the full workload when it is cheap, else N' = max(64 x cores, 4096) variants
+    n_s = n if est_s <= 30.0 else min(n, max(64 * cores, 4096))
+    seeds = np.arange(n_s, dtype=np.uint64)
+    walls = []
+    for _ in range(reps):
+        rc, out, wall, _, msg = O.ref_cpu_run(model_idx, seeds, sim_steps, workers=0)
+        if rc != 0:
+            raise RuntimeError("reference cpu_executor failed: " + msg)
+        walls.append(wall)
+    best = min(walls)
+    return {"value": n_s * sim_steps / best, "unit": "variant-steps/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"{MODELS[model_idx]} {n_s} variants x {sim_steps} steps, seeds 0..{n_s - 1}, "
+                      f"reference cpu_executor(workers=0 -> {cores} threads), best of {reps}",
+            "walls_s": walls}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a, ws, rank):
+    if rank != 0:
+        return
+    import oracle as O
+    k = MODELS.index(a.model)
+    base = {"metric": METRIC, "impl": "reference", "unit": "variant-steps/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "dtype": "f64",
+            "data": "synthetic (seeds 0..N-1, build_model initial states)",
+            "config": {"workload": workload_name(a), "model": a.model,
+                       "variants_per_gpu": a.variants, "sim_steps": a.sim_steps}}
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "oracle/_ref/libhetbench_ref.so was not built"}))
+        return
+    cores = O.ref_hardware_concurrency()
+    n_total = a.variants * a.gpus
+    # bounded per-step sample: ~10 s of host time per step at most
+    per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[k]
+    max_vs = 10.0 * cores / (per_vs_core_ns * 1e-9)
+    n_s = n_total if n_total * a.sim_steps <= max_vs else max(64 * cores, int(max_vs // a.sim_steps))
+    n_s = min(n_s, n_total)
+    seeds = np.arange(n_s, dtype=np.uint64)
+    for _ in range(a.warmup):
+        O.ref_cpu_run(k, seeds, a.sim_steps, workers=0)
+    t0 = time.perf_counter()
+    walls = []
+    for _ in range(a.steps):
+        rc, _, wall, _, msg = O.ref_cpu_run(k, seeds, a.sim_steps, workers=0)
+        if rc != 0:
+            raise RuntimeError(msg)
+        walls.append(wall)
+    total = time.perf_counter() - t0
+    value = n_s * a.sim_steps * a.steps / total
+    sample = (f"{a.model} {n_s} of {n_total} variants x {a.sim_steps} steps per bench step, "
+              f"reference cpu_executor(workers=0 -> {cores} threads)")
+    base.update({"value": value, "ms_per_step": 1e3 * total / a.steps,
+                 "cpu_baseline": {"value": value, "unit": "variant-steps/s", "cores": cores,
+                                  "kind": "reference", "sample": sample},
+                 "e2e": {"value": value, "unit": "variant-steps/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0},
+                 "vs_baseline": None, "scaling": "weak"})
+    print(json.dumps(base))
+
+
+# ---------------------------------------------------------------------- ours
+def run_ours(a, ws, rank, local):
+    import torch
+    import paper_2502_11129_b200 as hb
+
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    kind = hb.parse_model_kind(a.model)
+
+    # Global batch + N-way splitter (equal calibrated GPUs -> equal shares).
+    n_total = a.variants * ws
+    shares = hb.plan_allocation_n([1.0] * ws, n_total)
+    begin = sum(shares[:rank])
+    seeds = np.arange(begin, begin + shares[rank], dtype=np.uint64)
+    n = len(seeds)
+
+    ex = hb.GpuExecutor(local)
+    ctx = ex.ctx
+    ext = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident kernel timing (value) ----
+    ctx.stage(kind, seeds)
+    with torch.cuda.stream(ext):
+        for _ in range(a.warmup):
+            flush.zero_()
+            ctx.launch(a.sim_steps)
+    ctx.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    ctx.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(ext):
+        for e0, e1 in evs:
+            flush.zero_()           # L2 flush, outside the event pair
+            e0.record(ext)
+            ctx.launch(a.sim_steps)
+            e1.record(ext)
+    ctx.synchronize()
+    torch.cuda.synchronize(dev)
+    barrier()
+    wall_region = time.perf_counter() - t0
+    clk = clocks.stop()
+    kernel_ms = [e0.elapsed_time(e1) for e0, e1 in evs]
+    sum_ms = max_over_ranks(sum(kernel_ms))
+    ms_per_step = sum_ms / a.steps
+    units = n_total * a.sim_steps  # variant-steps per bench step, all ranks
+    value = units / (ms_per_step * 1e-3)
+    out, fail = ctx.fetch()
+    assert int(np.sum(fail)) == 0, "blow-up in bench workload"
+
+    # ---- roofline: FP64 pipe (measured probe on this device) ----
+    peak_ops, _ = ctx.fp64_peak()
+    per_gpu_rate = n * a.sim_steps / (float(np.mean(kernel_ms)) * 1e-3)
+    achieved = W_ALG[a.model] * per_gpu_rate
+    traffic = load_traffic(a.model, a.variants, a.sim_steps)
+    roof = {"bound": "fp64", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+            "unit": "TFLOP/s", "frac": achieved / peak_ops, "traffic": traffic,
+            "algorithmic_ops_per_variant_step": W_ALG[a.model],
+            "peak_source": "measured on this device by hb_fp64_peak (DMUL+DADD stream, no FMA); "
+                           "MEASURED_PEAKS.json has no FP64 figure",
+            "kernel": hb.kernel_name(kind, n),
+            "kernel_ms_mean": float(np.mean(kernel_ms)),
+            "hbm_bytes_per_launch_algorithmic":
+                n * (8 * (6 * BODIES[a.model] + CONS[a.model]) + 8 + 32 + 8)}
+
+    # ---- e2e through the drop-in call (host seeds -> host results) ----
+    e2e = None
+    if not a.no_e2e:
+        req = hb.BatchRequest(kind, seeds, a.sim_steps)
+        for _ in range(a.warmup):
+            ex.run(req)
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            r = ex.run(req)
+        t_e2e = time.perf_counter() - t0
+        barrier()
+        t_e2e = max_over_ranks(t_e2e)
+        assert np.array_equal(r.results, out)
+        rows = 6 * BODIES[a.model] + CONS[a.model]
+        e2e = {"value": units * a.steps / t_e2e, "unit": "variant-steps/s",
+               "h2d_bytes_per_step": n_total * (8 * rows + 8),
+               "d2h_bytes_per_step": n_total * (32 + 8),
+               "ms_per_step": 1e3 * t_e2e / a.steps,
+               "path": "GpuExecutor.run -> hb_run_batch (host init + H2D + kernel + D2H)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_rate(int(kind), n, a.sim_steps)
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"error": str(exc)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "variant-steps/s", "n_gpus": ws,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeds 0..N-1 through build_model; no datasets)",
+                "config": {"workload": workload_name(a), "model": a.model,
+                           "variants_per_gpu": a.variants, "global_variants": n_total,
+                           "sim_steps": a.sim_steps,
+                           "parallelism": f"dp{ws} (independent variants; contiguous slices "
+                                          "from plan_allocation_n)",
+                           "l2": "flushed between timed launches (256 MiB write outside the "
+                                 "event pair)"},
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+                "gpu_launches": a.steps, "e2e_gpu_launches": a.steps if e2e else 0,
+                "bracket_wall_s": wall_region, "parity": "bit-exact FP64 vs reference"}
+        print(json.dumps(line))
+    ex.ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    ws, rank, local = dist_env()
+    if a.impl == "reference":
+        run_reference(a, ws, rank)
+        return
+    run_ours(a, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/*
+ * hbgpu.h — C ABI of the B200-native batched variant-simulation backend.
+ *
+ * This is the drop-in boundary for the reference's accelerator slot
+ * (/root/reference/proj):
+ *
+ *   hetbench::batch_executor::run(const BatchRequest&) -> BatchResult
+ *       include/hetbench/executor.hpp:68-73
+ *   currently filled by synthetic_executor::run     src/executor.cpp:137-170
+ *   per variant: simulate(kind, seed, steps)         src/simkernel.cpp:187-203
+ *
+ * A reference-side adapter (include/hbgpu/hetbench_gpu_executor.hpp, shown in
+ * INTEGRATION.md) derives from hetbench::batch_executor and forwards run()
+ * to hb_run_batch(); nothing else in the reference changes.
+ *
+ * Rules: plain C types only; no exception crosses this boundary; every call
+ * returns an hb_status and the context keeps the last error message.  One
+ * context per device; a context is single-threaded (callers serialise per
+ * context), distinct contexts may be driven from distinct host threads
+ * concurrently (run_hybrid runs the accelerator share on a helper
+ * std::thread, src/scheduler.cpp:148-153).  There is no CPU fallback: on a
+ * host without a usable sm_100 device hb_ctx_create fails with
+ * HB_NO_DEVICE.
+ */
+#ifndef HBGPU_H
+#define HBGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HBGPU_ABI_VERSION 1
+
+/* hetbench::ModelKind (include/hetbench/simkernel.hpp:14) — same ordinals. */
+typedef enum {
+    HB_BOX = 0,
+    HB_BOX_AND_BALL = 1,
+    HB_ARM_WITH_ROPE = 2,
+    HB_HUMANOID = 3
+} hb_model_kind;
+
+typedef enum {
+    HB_OK = 0,
+    HB_INVALID_ARG = 1,    /* std::invalid_argument in the reference (executor.cpp:60-65) */
+    HB_CUDA_ERROR = 2,     /* device/runtime failure: the back-end is dead to calibrate() */
+    HB_BLOWUP_PARTIAL = 3, /* some variants blew up; the rest completed (batch_failure) */
+    HB_NO_DEVICE = 4       /* no usable sm_100 device */
+} hb_status;
+
+/* Byte-for-byte hetbench::VariantResult (simkernel.hpp:51-58): 32 B POD. */
+typedef struct {
+    uint64_t seed;
+    double fitness;
+    uint64_t checksum;
+    uint64_t steps_executed;
+} hb_variant_result;
+
+/* hetbench::AllocationPlan (scheduler.hpp:24-30). */
+typedef struct {
+    uint64_t n_total;
+    uint64_t n_cpu;
+    uint64_t n_accel;
+    double accel_fraction;
+    double requested_accel_fraction;
+} hb_allocation_plan;
+
+typedef struct hb_ctx hb_ctx;
+
+/* ---- library / model introspection ------------------------------------- */
+int hb_abi_version(void);
+/* Number of CUDA devices visible (0 when none / driver missing). */
+int hb_device_count(void);
+/* body_count (simkernel.hpp:23-31) and the constraint count of build_model
+ * (simkernel.cpp:95-118); -1 for an unknown kind. */
+int hb_body_count(int kind);
+int hb_constraint_count(int kind);
+/* Rows of the structure-of-arrays state for `kind`: 3n positions (body-major,
+ * x,y,z), 3n velocities, m rest lengths.  Row r of variant i lives at
+ * soa[r * ld + i]. */
+int hb_state_rows(int kind);
+/* Last error of calls that have no context (thread-local). */
+const char* hb_global_error(void);
+
+/* ---- context -------------------------------------------------------------- */
+hb_status hb_ctx_create(int device, hb_ctx** out);
+void hb_ctx_destroy(hb_ctx* ctx);
+const char* hb_last_error(const hb_ctx* ctx);
+int hb_ctx_device(const hb_ctx* ctx);
+/* The cudaStream_t every launch of this context is issued on. */
+void* hb_ctx_stream(hb_ctx* ctx);
+/* Host threads used by the host-side initialiser (default: all hardware
+ * threads, capped at 64). 0 = default. */
+hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
+
+/* ---- the drop-in call ------------------------------------------------------
+ * batch_executor::run (executor.hpp:70) for `n` seeds through `steps` fixed
+ * dt = kSimDt steps.  out[i] is the VariantResult of seeds[i] (seed order);
+ * fail_step[i] = 0 when variant i completed, otherwise the 1-based step whose
+ * end-of-step check raised numerical_blowup (simkernel.cpp:165-169), and
+ * out[i] is then unspecified.  Returns HB_BLOWUP_PARTIAL when any variant
+ * failed.  *wall_time_s (nullable) = steady-clock seconds around the whole
+ * call including host init, H2D and D2H (executor.cpp:91-115 semantics).
+ * fail_step may be NULL only if the caller does not need failure detail. */
+hb_status hb_run_batch(hb_ctx* ctx, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
+                       hb_variant_result* out, uint64_t* fail_step, double* wall_time_s);
+
+/* Host-side initialiser: build_model (simkernel.cpp:59-120) for each seed,
+ * written as SoA rows (hb_state_rows(kind) rows, leading dimension ld >= n). */
+hb_status hb_build_states(int kind, const uint64_t* seeds, size_t n, double* soa, size_t ld);
+
+/* Run from caller-supplied initial states (host SoA, ld = n) with step size
+ * dt (> 0, else HB_INVALID_ARG as step() throws at simkernel.cpp:123).
+ * seeds (nullable) only fill out[i].seed.  final_soa (nullable, ld = n)
+ * receives the final positions/velocities rows (rest rows copied through). */
+hb_status hb_run_states(hb_ctx* ctx, int kind, const double* init_soa, size_t n, uint64_t steps,
+                        double dt, const uint64_t* seeds, hb_variant_result* out,
+                        uint64_t* fail_step, double* final_soa);
+
+/* ---- device-resident (staged) path used for kernel-only timing ------------
+ * hb_stage: host init + H2D into the context's device buffers (synchronous).
+ * hb_launch: enqueue one stepping kernel over the staged batch on the
+ *   context stream (asynchronous; the staged inputs are not modified, so it
+ *   can be re-launched).
+ * hb_fetch: D2H of the last launch's results (synchronous). */
+hb_status hb_stage(hb_ctx* ctx, int kind, const uint64_t* seeds, size_t n);
+hb_status hb_launch(hb_ctx* ctx, uint64_t steps);
+hb_status hb_synchronize(hb_ctx* ctx);
+hb_status hb_fetch(hb_ctx* ctx, hb_variant_result* out, uint64_t* fail_step);
+/* Kernel variant the dispatcher picks for (kind, n): written to buf. */
+hb_status hb_kernel_name(int kind, size_t n, char* buf, size_t cap);
+
+/* ---- failure messages ------------------------------------------------------
+ * The what() of the numerical_blowup simulate() re-throws
+ * (simkernel.cpp:167-168,194):
+ *   "coordinate left the stable regime at t=<std::to_string(time)> (seed S)"
+ * where time is the FP64 running sum of dt after fail_step steps. */
+int hb_format_blowup(uint64_t seed, uint64_t fail_step, double dt, char* buf, size_t cap);
+
+/* ---- splitter (paper §6, scheduler.cpp:58-87) ----------------------------
+ * plan_allocation bit-for-bit (n_total >= 1). */
+hb_status hb_plan_allocation(double t_cpu_s, double t_accel_s, int cpu_ok, int accel_ok,
+                             uint64_t n_total, hb_allocation_plan* out);
+/* N-way "peeling" generalisation across `count` back-ends with calibrated
+ * probe times t_s[d] (ok[d] = 0 marks a dead back-end): for d = count-1..1,
+ * share[d] = plan_allocation({t_cpu = T_rest, t_accel = t_s[d]}, remaining)
+ * .n_accel, T_rest = t_s[0] when only back-end 0 remains, else
+ * 1 / sum_{j<d} 1/t_s[j]; back-end 0 takes the remainder.  For count == 2
+ * this is plan_allocation exactly (shares[0] = n_cpu, shares[1] = n_accel). */
+hb_status hb_plan_allocation_n(const double* t_s, const int* ok, int count, uint64_t n_total,
+                               uint64_t* shares);
+
+/* ---- multi-device executor -------------------------------------------------
+ * One context and one host thread per device; the batch is cut into
+ * contiguous slices (shares[d] variants to device d, in device order, as
+ * run_hybrid slices seeds at scheduler.cpp:122-127) and merged in seed order.
+ * shares == NULL splits evenly.  per_device_wall_s (nullable, `count`
+ * entries) receives each device's run wall time. */
+hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* shares, int kind,
+                             const uint64_t* seeds, size_t n, uint64_t steps,
+                             hb_variant_result* out, uint64_t* fail_step,
+                             double* per_device_wall_s, double* wall_time_s);
+
+/* ---- FP64 pipe peak probe (roofline denominator) ---------------------------
+ * Times a dependent-chain-free DADD/DMUL stream on the context's device and
+ * returns the sustained non-FMA FP64 op rate (ops/s) and the kernel time. */
+hb_status hb_fp64_peak(hb_ctx* ctx, double* ops_per_s, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HBGPU_H */

@@ -1,0 +1,88 @@
+"""ctypes binding of the C ABI in include/hbgpu.h (libhbgpu.so, built in-tree).
+
+The product has no CPU fallback: if the shared library is missing this module
+raises at import time, and a context cannot be created without an sm_100
+device (HB_NO_DEVICE).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libhbgpu.so")
+
+HB_OK, HB_INVALID_ARG, HB_CUDA_ERROR, HB_BLOWUP_PARTIAL, HB_NO_DEVICE = range(5)
+
+RESULT_DTYPE = np.dtype([("seed", "<u8"), ("fitness", "<f8"), ("checksum", "<u8"),
+                         ("steps_executed", "<u8")])
+
+# Every symbol include/hbgpu.h declares (checked by tests/test_abi.py).
+EXPORTED = (
+    "hb_abi_version", "hb_device_count", "hb_body_count", "hb_constraint_count",
+    "hb_state_rows", "hb_global_error", "hb_ctx_create", "hb_ctx_destroy", "hb_last_error",
+    "hb_ctx_device", "hb_ctx_stream", "hb_ctx_set_host_threads", "hb_run_batch",
+    "hb_build_states", "hb_run_states", "hb_stage", "hb_launch", "hb_synchronize", "hb_fetch",
+    "hb_kernel_name", "hb_format_blowup", "hb_plan_allocation", "hb_plan_allocation_n",
+    "hb_run_batch_multi", "hb_fp64_peak",
+)
+
+
+class Plan(C.Structure):
+    _fields_ = [("n_total", C.c_uint64), ("n_cpu", C.c_uint64), ("n_accel", C.c_uint64),
+                ("accel_fraction", C.c_double), ("requested_accel_fraction", C.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(make -C paper_2502_11129_b200/csrc). There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    u64, dbl, i32, sz, vp = C.c_uint64, C.c_double, C.c_int, C.c_size_t, C.c_void_p
+    P = C.POINTER
+    sig = {
+        "hb_abi_version": (i32, []),
+        "hb_device_count": (i32, []),
+        "hb_body_count": (i32, [i32]),
+        "hb_constraint_count": (i32, [i32]),
+        "hb_state_rows": (i32, [i32]),
+        "hb_global_error": (C.c_char_p, []),
+        "hb_ctx_create": (i32, [i32, P(vp)]),
+        "hb_ctx_destroy": (None, [vp]),
+        "hb_last_error": (C.c_char_p, [vp]),
+        "hb_ctx_device": (i32, [vp]),
+        "hb_ctx_stream": (vp, [vp]),
+        "hb_ctx_set_host_threads": (i32, [vp, i32]),
+        "hb_run_batch": (i32, [vp, i32, vp, sz, u64, vp, vp, P(dbl)]),
+        "hb_build_states": (i32, [i32, vp, sz, vp, sz]),
+        "hb_run_states": (i32, [vp, i32, vp, sz, u64, dbl, vp, vp, vp, vp]),
+        "hb_stage": (i32, [vp, i32, vp, sz]),
+        "hb_launch": (i32, [vp, u64]),
+        "hb_synchronize": (i32, [vp]),
+        "hb_fetch": (i32, [vp, vp, vp]),
+        "hb_kernel_name": (i32, [i32, sz, C.c_char_p, sz]),
+        "hb_format_blowup": (i32, [u64, u64, dbl, C.c_char_p, sz]),
+        "hb_plan_allocation": (i32, [dbl, dbl, i32, i32, u64, P(Plan)]),
+        "hb_plan_allocation_n": (i32, [vp, vp, i32, u64, vp]),
+        "hb_run_batch_multi": (i32, [vp, i32, vp, i32, vp, sz, u64, vp, vp, vp, P(dbl)]),
+        "hb_fp64_peak": (i32, [vp, P(dbl), P(dbl)]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def global_error() -> str:
+    return (lib.hb_global_error() or b"").decode()

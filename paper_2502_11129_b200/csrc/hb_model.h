@@ -1,0 +1,79 @@
+// hb_model.h — model definitions shared by the host initialiser and the
+// sm_100a stepping kernels.  Compile-time topology so every kernel is fully
+// specialised per ModelKind.
+//
+// Restates (does not include) the reference's constants and topology:
+//   kSimDt / kGravity / kProjectionIterations / kBlowupLimit  simkernel.hpp:67-71
+//   kStiffLink / kSoftLink                                    simkernel.cpp:13-14
+//   body_count                                                simkernel.hpp:23-31
+//   constraint lists (add_chain + switch)                     simkernel.cpp:35-40,95-118
+//   rng::mix64 / rng::at / rng::to_unit                       rng.hpp:15-32
+#pragma once
+
+#include <stdint.h>
+
+#if defined(__CUDACC__)
+#define HB_HD __host__ __device__ __forceinline__
+#else
+#define HB_HD inline
+#endif
+
+namespace hb {
+
+constexpr double kSimDt = 0.002;
+constexpr double kGravity = 9.81;
+constexpr int kIters = 8;
+constexpr double kBlowupLimit = 1e6;
+constexpr double kDamping = 0.8;  // build_model, simkernel.cpp:62
+constexpr double kStiffLink = 2.5e5;
+constexpr double kSoftLink = 1.25e5;
+constexpr double kMinDist = 1e-12;  // simkernel.cpp:144
+
+enum Kind : int { Box = 0, BoxAndBall = 1, ArmWithRope = 2, Humanoid = 3 };
+
+HB_HD constexpr int bodies(int k) { return k == 0 ? 1 : k == 1 ? 2 : k == 2 ? 12 : k == 3 ? 32 : 0; }
+HB_HD constexpr int constraints(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 11 : k == 3 ? 46 : 0; }
+HB_HD constexpr int state_rows(int k) { return 6 * bodies(k) + constraints(k); }
+
+// Constraint c of model k: endpoints (a, b) and whether it is a soft link.
+HB_HD constexpr int con_a(int k, int c) {
+    return k == 3 ? (c < 15 ? c : c < 30 ? c + 1 : c - 30) : c;
+}
+HB_HD constexpr int con_b(int k, int c) {
+    return k == 3 ? (c < 15 ? c + 1 : c < 30 ? c + 2 : c - 30 + 16) : c + 1;
+}
+HB_HD constexpr bool con_soft(int k, int c) { return k == 2 && c >= 5; }
+
+// ---- counter-based generator (rng.hpp:15-32) ----
+HB_HD constexpr uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xBF58476D1CE4E5B9ull;
+    x ^= x >> 27;
+    x *= 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    return x;
+}
+HB_HD constexpr uint64_t rng_at(uint64_t key, uint64_t ctr) {
+    return mix64(mix64(key + 0x9E3779B97F4A7C15ull) ^ (ctr * 0xD1B54A32D192ED03ull + 1));
+}
+HB_HD constexpr double to_unit(uint64_t bits) { return static_cast<double>(bits >> 11) * 0x1.0p-53; }
+
+// EA keys (ea.cpp:15-16)
+constexpr uint64_t kInitKey = 0x8F5D4C3B2A190807ull;
+constexpr uint64_t kChildKey = 0x243F6A8885A308D3ull;
+
+// ---- FNV-1a 64 (simkernel.cpp:16-26) ----
+constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
+constexpr uint64_t kFnvPrime = 0x100000001b3ull;
+HB_HD uint64_t fnv_absorb_bits(uint64_t h, uint64_t bits) {
+#if defined(__CUDACC__)
+#pragma unroll
+#endif
+    for (int i = 0; i < 8; ++i) {
+        h ^= (bits >> (8 * i)) & 0xffu;
+        h *= kFnvPrime;
+    }
+    return h;
+}
+
+}  // namespace hb

@@ -1,0 +1,644 @@
+// hb_runtime.cpp — host runtime behind the C ABI (include/hbgpu.h).
+//
+//  * host initialiser: build_model (reference src/simkernel.cpp:59-120)
+//    written straight into pinned structure-of-arrays rows by a persistent
+//    thread pool.  It stays on the host on purpose: glibc cos/sin are the only
+//    bit-exact source of the initial arc;
+//  * per-device context: stream, device + pinned buffers grown on demand;
+//  * hb_run_batch = validate -> init -> H2D -> persistent kernel -> D2H,
+//    the batch_executor::run contract (executor.hpp:68-73);
+//  * the paper's reverse-ratio splitter, bit-for-bit (scheduler.cpp:58-87),
+//    and its N-way generalisation plus a one-thread-per-device executor.
+//
+// Built with -O3 -ffp-contract=off (no FMA contraction: the initialiser must
+// match the reference's IEEE double operation order).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "hb_internal.h"
+#include "hb_model.h"
+
+namespace {
+
+thread_local std::string g_error;
+
+hb_status set_global(hb_status st, const std::string& msg) {
+    g_error = msg;
+    return st;
+}
+
+bool valid_kind(int kind) { return kind >= 0 && kind <= 3; }
+
+// ---------------------------------------------------------------------------
+// Persistent fork/join pool.  The caller thread takes part; work is handed
+// out in contiguous chunks (like cpu_executor, executor.cpp:93-113).
+class ThreadPool {
+public:
+    explicit ThreadPool(int threads) : n_(std::max(1, threads)) {
+        for (int t = 1; t < n_; ++t) workers_.emplace_back([this, t] { loop(t); });
+    }
+    ~ThreadPool() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& w : workers_) w.join();
+    }
+    int size() const { return n_; }
+
+    // fn(begin, end) over [0, total) split into `parts` contiguous chunks.
+    void run(size_t total, const std::function<void(size_t, size_t)>& fn) {
+        if (total == 0) return;
+        const int parts = static_cast<int>(std::min<size_t>(n_, total));
+        if (parts == 1) {
+            fn(0, total);
+            return;
+        }
+        std::unique_lock<std::mutex> lk(m_);
+        fn_ = &fn;
+        total_ = total;
+        parts_ = parts;
+        next_.store(0);
+        done_ = 0;
+        ++gen_;
+        lk.unlock();
+        cv_.notify_all();
+        work();
+        lk.lock();
+        done_cv_.wait(lk, [&] { return done_ == parts_; });
+        fn_ = nullptr;
+    }
+
+private:
+    void work() {
+        for (;;) {
+            const int part = next_.fetch_add(1);
+            if (part >= parts_) break;
+            const size_t chunk = total_ / parts_, extra = total_ % parts_;
+            const size_t b = part * chunk + std::min<size_t>(part, extra);
+            const size_t e = b + chunk + (static_cast<size_t>(part) < extra ? 1 : 0);
+            (*fn_)(b, e);
+            std::lock_guard<std::mutex> g(m_);
+            if (++done_ == parts_) done_cv_.notify_all();
+        }
+    }
+    void loop(int) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(m_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+            if (stop_) return;
+            if (!fn_) continue;
+            lk.unlock();
+            work();
+        }
+    }
+    int n_;
+    std::vector<std::thread> workers_;
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    const std::function<void(size_t, size_t)>* fn_ = nullptr;
+    size_t total_ = 0;
+    int parts_ = 0;
+    std::atomic<int> next_{0};
+    int done_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+int default_host_threads() {
+    unsigned hc = std::thread::hardware_concurrency();
+    return static_cast<int>(std::min(64u, std::max(1u, hc)));
+}
+
+// ---------------------------------------------------------------------------
+// build_model (simkernel.cpp:59-120) for one variant into SoA rows.
+struct Stream {
+    uint64_t key, ctr;
+    double unit() { return hb::to_unit(hb::rng_at(key, ctr++)); }
+    double range(double lo, double hi) { return lo + (hi - lo) * unit(); }  // rng.hpp:44
+};
+
+template <int K>
+void build_one(uint64_t seed, double* soa, size_t ld, size_t i) {
+    constexpr int n = hb::bodies(K);
+    constexpr int m = hb::constraints(K);
+    constexpr bool twin = (K == hb::Humanoid);
+    Stream rs{seed, 0};
+    const double drop_height = rs.range(0.5, 2.0);
+    const double lx = rs.range(-1.0, 1.0);
+    const double ly = rs.range(-1.0, 1.0);
+    const double heading = rs.range(0.0, 2.0 * 3.14159265358979323846);
+    const double spacing = twin ? 0.12 : 0.25;
+    double px[n], py[n], pz[n];
+    for (int b = 0; b < n; ++b) {
+        const int j = twin ? b % 16 : b;
+        const double a = heading + 0.15 * static_cast<double>(j);
+        const double ca = std::cos(a), sa = std::sin(a);
+        double x = spacing * static_cast<double>(j) * ca;
+        double y = spacing * static_cast<double>(j) * sa;
+        double z = drop_height + 0.05 * static_cast<double>(j);
+        if (twin && b >= 16) {  // rail B offset (:85-89)
+            x -= spacing * sa;
+            y += spacing * ca;
+        }
+        x += 1e-3 * rs.range(-1.0, 1.0);
+        y += 1e-3 * rs.range(-1.0, 1.0);
+        z += 1e-3 * rs.unit();
+        px[b] = x; py[b] = y; pz[b] = z;
+        soa[(3 * b + 0) * ld + i] = x;
+        soa[(3 * b + 1) * ld + i] = y;
+        soa[(3 * b + 2) * ld + i] = z;
+        soa[(3 * n + 3 * b + 0) * ld + i] = lx;
+        soa[(3 * n + 3 * b + 1) * ld + i] = ly;
+        soa[(3 * n + 3 * b + 2) * ld + i] = 0.0;
+    }
+    for (int c = 0; c < m; ++c) {  // rest = initial distance (add_chain :35-40, rungs :112-115)
+        const int A = hb::con_a(K, c), B = hb::con_b(K, c);
+        const double dx = px[B] - px[A], dy = py[B] - py[A], dz = pz[B] - pz[A];
+        soa[(6 * n + c) * ld + i] = std::sqrt(dx * dx + dy * dy + dz * dz);
+    }
+}
+
+void build_range(int kind, const uint64_t* seeds, size_t b, size_t e, double* soa, size_t ld) {
+    switch (kind) {
+        case 0: for (size_t i = b; i < e; ++i) build_one<0>(seeds[i], soa, ld, i); break;
+        case 1: for (size_t i = b; i < e; ++i) build_one<1>(seeds[i], soa, ld, i); break;
+        case 2: for (size_t i = b; i < e; ++i) build_one<2>(seeds[i], soa, ld, i); break;
+        case 3: for (size_t i = b; i < e; ++i) build_one<3>(seeds[i], soa, ld, i); break;
+    }
+}
+
+double elapsed_s(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct hb_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    ThreadPool* pool = nullptr;
+    int host_threads = 0;
+
+    // device buffers
+    double* d_init = nullptr;
+    size_t d_init_cap = 0;  // doubles
+    uint64_t* d_seeds = nullptr;
+    hb_variant_result* d_out = nullptr;
+    uint64_t* d_fail = nullptr;
+    size_t d_n_cap = 0;
+    double* d_final = nullptr;
+    size_t d_final_cap = 0;
+    double* d_scratch = nullptr;
+
+    // pinned host buffers
+    double* h_init = nullptr;
+    size_t h_init_cap = 0;
+    uint64_t* h_seeds = nullptr;
+    hb_variant_result* h_out = nullptr;
+    uint64_t* h_fail = nullptr;
+    size_t h_n_cap = 0;
+
+    // staged batch
+    int staged_kind = -1;
+    size_t staged_n = 0;
+
+    hb_status fail(hb_status st, const std::string& msg) {
+        err = msg;
+        g_error = msg;
+        return st;
+    }
+    hb_status cuda(cudaError_t e, const char* what) {
+        if (e == cudaSuccess) return HB_OK;
+        return fail(HB_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+};
+
+namespace {
+
+#define HB_TRY(expr)                          \
+    do {                                      \
+        hb_status _st = (expr);               \
+        if (_st != HB_OK) return _st;         \
+    } while (0)
+
+hb_status ensure_capacity(hb_ctx* c, int kind, size_t n) {
+    const size_t rows = static_cast<size_t>(hb::state_rows(kind));
+    const size_t need = rows * n;
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    if (need > c->d_init_cap) {
+        if (c->d_init) cudaFree(c->d_init);
+        c->d_init = nullptr;
+        const size_t cap = std::max(need, c->d_init_cap * 2);
+        HB_TRY(c->cuda(cudaMalloc(&c->d_init, cap * sizeof(double)), "cudaMalloc(init)"));
+        c->d_init_cap = cap;
+    }
+    if (need > c->h_init_cap) {
+        if (c->h_init) cudaFreeHost(c->h_init);
+        c->h_init = nullptr;
+        const size_t cap = std::max(need, c->h_init_cap * 2);
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_init, cap * sizeof(double), cudaHostAllocPortable),
+                       "cudaHostAlloc(init)"));
+        c->h_init_cap = cap;
+    }
+    if (n > c->d_n_cap) {
+        cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
+        c->d_seeds = nullptr; c->d_out = nullptr; c->d_fail = nullptr;
+        const size_t cap = std::max(n, c->d_n_cap * 2);
+        HB_TRY(c->cuda(cudaMalloc(&c->d_seeds, cap * sizeof(uint64_t)), "cudaMalloc(seeds)"));
+        HB_TRY(c->cuda(cudaMalloc(&c->d_out, cap * sizeof(hb_variant_result)), "cudaMalloc(out)"));
+        HB_TRY(c->cuda(cudaMalloc(&c->d_fail, cap * sizeof(uint64_t)), "cudaMalloc(fail)"));
+        c->d_n_cap = cap;
+    }
+    if (n > c->h_n_cap) {
+        cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
+        c->h_seeds = nullptr; c->h_out = nullptr; c->h_fail = nullptr;
+        const size_t cap = std::max(n, c->h_n_cap * 2);
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_seeds, cap * sizeof(uint64_t), 0), "cudaHostAlloc(seeds)"));
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_out, cap * sizeof(hb_variant_result), 0), "cudaHostAlloc(out)"));
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_fail, cap * sizeof(uint64_t), 0), "cudaHostAlloc(fail)"));
+        c->h_n_cap = cap;
+    }
+    return HB_OK;
+}
+
+ThreadPool& pool_of(hb_ctx* c) {
+    if (!c->pool) c->pool = new ThreadPool(c->host_threads > 0 ? c->host_threads : default_host_threads());
+    return *c->pool;
+}
+
+hb_status validate(hb_ctx* c, int kind, const void* seeds, size_t n, uint64_t steps, const void* out) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (!valid_kind(kind)) return c->fail(HB_INVALID_ARG, "unknown model kind " + std::to_string(kind));
+    if (n == 0) return c->fail(HB_INVALID_ARG, "batch request: seeds must be non-empty");
+    if (steps < 1) return c->fail(HB_INVALID_ARG, "batch request: steps must be >= 1");
+    if (!seeds || !out) return c->fail(HB_INVALID_ARG, "null buffer");
+    return HB_OK;
+}
+
+// Host init of `n` seeds into the pinned SoA image + async H2D of state and seeds.
+hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
+    HB_TRY(ensure_capacity(c, kind, n));
+    std::memcpy(c->h_seeds, seeds, n * sizeof(uint64_t));
+    double* soa = c->h_init;
+    pool_of(c).run(n, [&](size_t b, size_t e) { build_range(kind, seeds, b, e, soa, n); });
+    const size_t rows = static_cast<size_t>(hb::state_rows(kind));
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
+                                   cudaMemcpyHostToDevice, c->stream), "H2D init"));
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, c->h_seeds, n * sizeof(uint64_t),
+                                   cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+    return HB_OK;
+}
+
+hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, double* d_final) {
+    hb::SimArgs a{c->d_init, n, n, steps, dt, c->d_seeds, c->d_out, c->d_fail, d_final};
+    return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms), "kernel launch");
+}
+
+hb_status fetch(hb_ctx* c, size_t n, hb_variant_result* out, uint64_t* fail_step, bool* any_fail) {
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_out, c->d_out, n * sizeof(hb_variant_result),
+                                   cudaMemcpyDeviceToHost, c->stream), "D2H results"));
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_fail, c->d_fail, n * sizeof(uint64_t),
+                                   cudaMemcpyDeviceToHost, c->stream), "D2H status"));
+    HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+    std::memcpy(out, c->h_out, n * sizeof(hb_variant_result));
+    bool any = false;
+    for (size_t i = 0; i < n; ++i) any |= (c->h_fail[i] != 0);
+    if (fail_step) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
+    *any_fail = any;
+    return HB_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int hb_abi_version(void) { return HBGPU_ABI_VERSION; }
+
+int hb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int hb_body_count(int kind) { return valid_kind(kind) ? hb::bodies(kind) : -1; }
+int hb_constraint_count(int kind) { return valid_kind(kind) ? hb::constraints(kind) : -1; }
+int hb_state_rows(int kind) { return valid_kind(kind) ? hb::state_rows(kind) : -1; }
+const char* hb_global_error(void) { return g_error.c_str(); }
+
+hb_status hb_ctx_create(int device, hb_ctx** out) {
+    if (!out) return set_global(HB_INVALID_ARG, "null output pointer");
+    *out = nullptr;
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return set_global(HB_NO_DEVICE, std::string("no CUDA device: ") +
+                                            (e != cudaSuccess ? cudaGetErrorString(e) : "count = 0"));
+    }
+    if (device < 0 || device >= count)
+        return set_global(HB_INVALID_ARG, "device ordinal out of range");
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+        return set_global(HB_NO_DEVICE, "cudaGetDeviceProperties failed");
+    if (prop.major != 10)
+        return set_global(HB_NO_DEVICE, "device is sm_" + std::to_string(prop.major) +
+                                            std::to_string(prop.minor) +
+                                            "; this build targets sm_100a only");
+    hb_ctx* c = new hb_ctx();
+    c->device = device;
+    c->sms = prop.multiProcessorCount;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaMalloc(&c->d_scratch, 64) != cudaSuccess) {
+        delete c;
+        return set_global(HB_CUDA_ERROR, "stream/scratch creation failed");
+    }
+    *out = c;
+    return HB_OK;
+}
+
+void hb_ctx_destroy(hb_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
+    cudaFree(c->d_final); cudaFree(c->d_scratch);
+    cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c->pool;
+    delete c;
+}
+
+const char* hb_last_error(const hb_ctx* c) { return c ? c->err.c_str() : g_error.c_str(); }
+int hb_ctx_device(const hb_ctx* c) { return c ? c->device : -1; }
+void* hb_ctx_stream(hb_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+hb_status hb_ctx_set_host_threads(hb_ctx* c, int threads) {
+    if (!c || threads < 0) return set_global(HB_INVALID_ARG, "bad arguments");
+    delete c->pool;
+    c->pool = nullptr;
+    c->host_threads = threads;
+    return HB_OK;
+}
+
+hb_status hb_build_states(int kind, const uint64_t* seeds, size_t n, double* soa, size_t ld) {
+    if (!valid_kind(kind)) return set_global(HB_INVALID_ARG, "unknown model kind");
+    if (!seeds || !soa || ld < n) return set_global(HB_INVALID_ARG, "bad buffers");
+    build_range(kind, seeds, 0, n, soa, ld);
+    return HB_OK;
+}
+
+hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
+                       hb_variant_result* out, uint64_t* fail_step, double* wall_time_s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    HB_TRY(validate(c, kind, seeds, n, steps, out));
+    HB_TRY(stage_inputs(c, kind, seeds, n));
+    HB_TRY(launch(c, kind, n, steps, hb::kSimDt, nullptr));
+    c->staged_kind = -1;  // d_init now holds this batch; not a staged launch target
+    bool any = false;
+    HB_TRY(fetch(c, n, out, fail_step, &any));
+    if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
+    if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_run_states(hb_ctx* c, int kind, const double* init_soa, size_t n, uint64_t steps,
+                        double dt, const uint64_t* seeds, hb_variant_result* out,
+                        uint64_t* fail_step, double* final_soa) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (!valid_kind(kind)) return c->fail(HB_INVALID_ARG, "unknown model kind");
+    if (!init_soa || !out || n == 0) return c->fail(HB_INVALID_ARG, "bad buffers");
+    if (steps < 1) return c->fail(HB_INVALID_ARG, "simulate: steps must be >= 1");
+    if (!(dt > 0.0)) return c->fail(HB_INVALID_ARG, "step: dt must be > 0");
+    HB_TRY(ensure_capacity(c, kind, n));
+    const size_t rows = static_cast<size_t>(hb::state_rows(kind));
+    const size_t bytes = rows * n * sizeof(double);
+    if (final_soa && rows * n > c->d_final_cap) {
+        cudaFree(c->d_final);
+        c->d_final = nullptr;
+        HB_TRY(c->cuda(cudaMalloc(&c->d_final, bytes), "cudaMalloc(final)"));
+        c->d_final_cap = rows * n;
+    }
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, init_soa, bytes, cudaMemcpyHostToDevice, c->stream), "H2D"));
+    if (seeds) {
+        HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, seeds, n * sizeof(uint64_t),
+                                       cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+    } else {
+        HB_TRY(c->cuda(cudaMemsetAsync(c->d_seeds, 0, n * sizeof(uint64_t), c->stream), "memset"));
+    }
+    c->staged_kind = -1;
+    HB_TRY(launch(c, kind, n, steps, dt, final_soa ? c->d_final : nullptr));
+    bool any = false;
+    HB_TRY(fetch(c, n, out, fail_step, &any));
+    if (final_soa) {
+        HB_TRY(c->cuda(cudaMemcpy(final_soa, c->d_final, bytes, cudaMemcpyDeviceToHost), "D2H final"));
+    }
+    if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_stage(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
+    HB_TRY(validate(c, kind, seeds, n, 1, seeds));
+    HB_TRY(stage_inputs(c, kind, seeds, n));
+    HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+    c->staged_kind = kind;
+    c->staged_n = n;
+    return HB_OK;
+}
+
+hb_status hb_launch(hb_ctx* c, uint64_t steps) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (c->staged_kind < 0) return c->fail(HB_INVALID_ARG, "hb_launch: no staged batch");
+    if (steps < 1) return c->fail(HB_INVALID_ARG, "batch request: steps must be >= 1");
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    return launch(c, c->staged_kind, c->staged_n, steps, hb::kSimDt, nullptr);
+}
+
+hb_status hb_synchronize(hb_ctx* c) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    return c->cuda(cudaStreamSynchronize(c->stream), "stream sync");
+}
+
+hb_status hb_fetch(hb_ctx* c, hb_variant_result* out, uint64_t* fail_step) {
+    if (!c || !out) return set_global(HB_INVALID_ARG, "bad arguments");
+    if (c->staged_kind < 0) return c->fail(HB_INVALID_ARG, "hb_fetch: no staged batch");
+    bool any = false;
+    HB_TRY(fetch(c, c->staged_n, out, fail_step, &any));
+    if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_kernel_name(int kind, size_t n, char* buf, size_t cap) {
+    if (!valid_kind(kind) || !buf || cap == 0) return set_global(HB_INVALID_ARG, "bad arguments");
+    std::snprintf(buf, cap, "%s", hb::kernel_name(kind, n));
+    return HB_OK;
+}
+
+int hb_format_blowup(uint64_t seed, uint64_t fail_step, double dt, char* buf, size_t cap) {
+    double t = 0.0;
+    for (uint64_t s = 0; s < fail_step; ++s) t += dt;  // WorldState::time += dt (:163)
+    const std::string msg = "coordinate left the stable regime at t=" + std::to_string(t) +
+                            " (seed " + std::to_string(seed) + ")";
+    if (buf && cap) std::snprintf(buf, cap, "%s", msg.c_str());
+    return static_cast<int>(msg.size());
+}
+
+// plan_allocation — scheduler.cpp:58-87, bit-for-bit.
+hb_status hb_plan_allocation(double t_cpu, double t_accel, int cpu_ok, int accel_ok,
+                             uint64_t n_total, hb_allocation_plan* out) {
+    if (!out) return set_global(HB_INVALID_ARG, "null plan");
+    if (n_total < 1) return set_global(HB_INVALID_ARG, "plan_allocation: n_total must be >= 1");
+    hb_allocation_plan p{};
+    p.n_total = n_total;
+    if (!accel_ok) {
+        p.n_accel = 0;
+    } else if (!cpu_ok) {
+        p.n_accel = n_total;
+        p.requested_accel_fraction = 1.0;
+    } else {
+        const double f = t_cpu / (t_cpu + t_accel);
+        p.requested_accel_fraction = f;
+        uint64_t na = static_cast<uint64_t>(std::llround(f * static_cast<double>(n_total)));
+        na = std::min(na, n_total);
+        const double thr = 1.0 / (2.0 * static_cast<double>(n_total));
+        if (na == 0 && f >= thr) na = 1;
+        if (na == n_total && (1.0 - f) >= thr) na = n_total - 1;
+        p.n_accel = na;
+    }
+    p.n_cpu = n_total - p.n_accel;
+    p.accel_fraction = static_cast<double>(p.n_accel) / static_cast<double>(n_total);
+    *out = p;
+    return HB_OK;
+}
+
+hb_status hb_plan_allocation_n(const double* t_s, const int* ok, int count, uint64_t n_total,
+                               uint64_t* shares) {
+    if (!t_s || !shares || count < 1) return set_global(HB_INVALID_ARG, "bad arguments");
+    if (n_total < 1) return set_global(HB_INVALID_ARG, "plan_allocation: n_total must be >= 1");
+    int alive = 0;
+    for (int d = 0; d < count; ++d) alive += (!ok || ok[d]) ? 1 : 0;
+    if (alive == 0) return set_global(HB_INVALID_ARG, "calibrate: all back-ends failed");
+    uint64_t remaining = n_total;
+    for (int d = count - 1; d >= 1; --d) {
+        const bool ok_d = !ok || ok[d];
+        // Aggregate of devices 0..d-1 (the "cpu" side of the 2-way plan).
+        bool rest_ok = false;
+        double inv_sum = 0.0;
+        int rest_alive = 0;
+        for (int j = 0; j < d; ++j)
+            if (!ok || ok[j]) {
+                rest_ok = true;
+                inv_sum += 1.0 / t_s[j];
+                ++rest_alive;
+            }
+        double t_rest = 0.0;
+        if (rest_alive == 1) {
+            for (int j = 0; j < d; ++j)
+                if (!ok || ok[j]) t_rest = t_s[j];
+        } else if (rest_alive > 1) {
+            t_rest = 1.0 / inv_sum;
+        }
+        if (remaining == 0) {
+            shares[d] = 0;
+            continue;
+        }
+        hb_allocation_plan p;
+        hb_plan_allocation(t_rest, t_s[d], rest_ok ? 1 : 0, ok_d ? 1 : 0, remaining, &p);
+        shares[d] = p.n_accel;
+        remaining -= p.n_accel;
+    }
+    shares[0] = remaining;
+    return HB_OK;
+}
+
+hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* shares, int kind,
+                             const uint64_t* seeds, size_t n, uint64_t steps,
+                             hb_variant_result* out, uint64_t* fail_step,
+                             double* per_device_wall_s, double* wall_time_s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!ctxs || count < 1) return set_global(HB_INVALID_ARG, "no contexts");
+    if (!valid_kind(kind)) return set_global(HB_INVALID_ARG, "unknown model kind");
+    if (n == 0) return set_global(HB_INVALID_ARG, "batch request: seeds must be non-empty");
+    if (steps < 1) return set_global(HB_INVALID_ARG, "batch request: steps must be >= 1");
+    std::vector<uint64_t> sh(count);
+    if (shares) {
+        uint64_t sum = 0;
+        for (int d = 0; d < count; ++d) sum += (sh[d] = shares[d]);
+        if (sum != n) return set_global(HB_INVALID_ARG, "shares do not sum to the batch size");
+    } else {
+        for (int d = 0; d < count; ++d) sh[d] = n / count + (static_cast<uint64_t>(d) < n % count ? 1 : 0);
+    }
+    std::vector<hb_status> st(count, HB_OK);
+    std::vector<double> walls(count, 0.0);
+    std::vector<std::thread> th;
+    size_t begin = 0;
+    for (int d = 0; d < count; ++d) {
+        const size_t b = begin, len = sh[d];
+        begin += len;
+        if (len == 0) continue;
+        th.emplace_back([&, d, b, len] {
+            st[d] = hb_run_batch(ctxs[d], kind, seeds + b, len, steps, out + b,
+                                 fail_step ? fail_step + b : nullptr, &walls[d]);
+        });
+    }
+    for (auto& t : th) t.join();
+    if (per_device_wall_s)
+        for (int d = 0; d < count; ++d) per_device_wall_s[d] = walls[d];
+    if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
+    bool blow = false;
+    for (int d = 0; d < count; ++d) {
+        if (st[d] == HB_BLOWUP_PARTIAL) blow = true;
+        else if (st[d] != HB_OK) return set_global(st[d], std::string("device ") + std::to_string(d) +
+                                                              ": " + hb_last_error(ctxs[d]));
+    }
+    if (blow) return set_global(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_fp64_peak(hb_ctx* c, double* ops_per_s, double* ms) {
+    if (!c || !ops_per_s) return set_global(HB_INVALID_ARG, "bad arguments");
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    double ops = 0.0;
+    const int iters = 4096;
+    hb::launch_fp64_probe(c->d_scratch, c->sms, iters, c->stream, &ops);  // warm-up
+    cudaEventRecord(e0, c->stream);
+    HB_TRY(c->cuda(hb::launch_fp64_probe(c->d_scratch, c->sms, iters, c->stream, &ops), "fp64 probe"));
+    cudaEventRecord(e1, c->stream);
+    HB_TRY(c->cuda(cudaEventSynchronize(e1), "event sync"));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ops_per_s = ops / (static_cast<double>(t) * 1e-3);
+    if (ms) *ms = t;
+    return HB_OK;
+}
+
+}  // extern "C"

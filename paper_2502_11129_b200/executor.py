@@ -1,0 +1,306 @@
+"""Executor boundary — Python mirror of hetbench's batch contract
+(/root/reference/proj/include/hetbench/executor.hpp:17-128) over the C ABI.
+
+``GpuExecutor`` is the B200 back-end that takes the accelerator slot
+(``synthetic_executor``, src/executor.cpp:137-170): ``run(BatchRequest)``
+returns a ``BatchResult`` whose results are bit-identical to the reference
+``simulate`` (src/simkernel.cpp:187-203) seed for seed, or raises
+``BatchFailure`` carrying the failed seeds (sorted) and the completed results,
+with the reference's message format (executor.cpp:20-28).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import RESULT_DTYPE, lib
+
+KSIM_DT = 0.002
+
+
+class ModelKind(enum.IntEnum):
+    """hetbench::ModelKind (simkernel.hpp:14), same ordinals."""
+    Box = 0
+    BoxAndBall = 1
+    ArmWithRope = 2
+    Humanoid = 3
+
+
+_NAMES = ("box", "box_and_ball", "arm_with_rope", "humanoid")
+ALL_MODELS = tuple(ModelKind)
+
+
+def to_string(kind: ModelKind) -> str:
+    return _NAMES[int(kind)]
+
+
+def parse_model_kind(name: str) -> ModelKind:
+    """simkernel.cpp:52-56."""
+    for k in ModelKind:
+        if _NAMES[int(k)] == name:
+            return k
+    raise ValueError(f"unknown model kind: {name}")
+
+
+def body_count(kind: ModelKind) -> int:
+    return int(lib.hb_body_count(int(kind)))
+
+
+def constraint_count(kind: ModelKind) -> int:
+    return int(lib.hb_constraint_count(int(kind)))
+
+
+def state_rows(kind: ModelKind) -> int:
+    return int(lib.hb_state_rows(int(kind)))
+
+
+class NumericalBlowup(RuntimeError):
+    """hetbench::numerical_blowup (simkernel.hpp:62-65)."""
+
+
+class BatchFailure(RuntimeError):
+    """hetbench::batch_failure (executor.hpp:34-45): failed = [(seed, message)]
+    sorted, completed = results of the variants that finished, in order."""
+
+    def __init__(self, failed, completed):
+        self.failed = sorted(failed)
+        self.completed = completed
+        first_seed, first_msg = self.failed[0]
+        msg = f"batch failed for seed {first_seed}"
+        if len(self.failed) > 1:
+            msg += f" (+{len(self.failed) - 1} more)"
+        msg += ": " + first_msg
+        super().__init__(msg)
+
+
+@dataclass
+class BatchRequest:
+    kind: ModelKind = ModelKind.Box
+    seeds: np.ndarray = field(default_factory=lambda: np.zeros(0, dtype=np.uint64))
+    steps: int = 1
+
+    def __post_init__(self):
+        self.kind = ModelKind(self.kind)
+        self.seeds = np.ascontiguousarray(np.asarray(self.seeds, dtype=np.uint64))
+
+
+@dataclass
+class BatchResult:
+    """results: structured array (seed, fitness, checksum, steps_executed),
+    request order — the 32-byte VariantResult layout."""
+    results: np.ndarray
+    wall_time_s: float = 0.0
+    utilization_trace: list = field(default_factory=list)
+
+
+def validate_request(request: BatchRequest) -> None:
+    """executor.cpp:60-65."""
+    if len(request.seeds) == 0:
+        raise ValueError("batch request: seeds must be non-empty")
+    if request.steps < 1:
+        raise ValueError("batch request: steps must be >= 1")
+
+
+def format_blowup(seed: int, fail_step: int, dt: float = KSIM_DT) -> str:
+    buf = C.create_string_buffer(256)
+    lib.hb_format_blowup(int(seed), int(fail_step), dt, buf, 256)
+    return buf.value.decode()
+
+
+def _raise_partial(seeds: np.ndarray, out: np.ndarray, fail: np.ndarray):
+    bad = np.nonzero(fail)[0]
+    failed = [(int(seeds[i]), format_blowup(int(seeds[i]), int(fail[i]))) for i in bad]
+    completed = out[fail == 0].copy()
+    raise BatchFailure(failed, completed)
+
+
+class BatchExecutor:
+    """hetbench::batch_executor (executor.hpp:68-73)."""
+
+    def run(self, request: BatchRequest) -> BatchResult:  # pragma: no cover - interface
+        raise NotImplementedError
+
+    def name(self) -> str:  # pragma: no cover - interface
+        raise NotImplementedError
+
+
+class DeviceContext:
+    """Owns one hb_ctx (one device, one stream, pinned + device buffers)."""
+
+    def __init__(self, device: int = 0, host_threads: int = 0):
+        h = C.c_void_p()
+        st = lib.hb_ctx_create(device, C.byref(h))
+        if st != _lib.HB_OK:
+            raise RuntimeError(f"hb_ctx_create({device}) failed [{st}]: {_lib.global_error()}")
+        self.handle = h.value
+        self.device = device
+        if host_threads:
+            lib.hb_ctx_set_host_threads(self.handle, host_threads)
+
+    def error(self) -> str:
+        return (lib.hb_last_error(self.handle) or b"").decode()
+
+    def check(self, st: int, what: str) -> None:
+        if st == _lib.HB_INVALID_ARG:
+            raise ValueError(self.error())
+        if st not in (_lib.HB_OK, _lib.HB_BLOWUP_PARTIAL):
+            raise RuntimeError(f"{what} failed [{st}]: {self.error()}")
+
+    @property
+    def stream(self) -> int:
+        return int(lib.hb_ctx_stream(self.handle) or 0)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib.hb_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- staged (device-resident) path, used by bench.py for kernel timing
+    def stage(self, kind: ModelKind, seeds: np.ndarray) -> None:
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        self._staged = seeds
+        self.check(lib.hb_stage(self.handle, int(kind), _lib.ptr(seeds), len(seeds)), "hb_stage")
+
+    def launch(self, steps: int) -> None:
+        self.check(lib.hb_launch(self.handle, steps), "hb_launch")
+
+    def synchronize(self) -> None:
+        self.check(lib.hb_synchronize(self.handle), "hb_synchronize")
+
+    def fetch(self):
+        n = len(self._staged)
+        out = np.zeros(n, dtype=RESULT_DTYPE)
+        fail = np.zeros(n, dtype=np.uint64)
+        self.check(lib.hb_fetch(self.handle, _lib.ptr(out), _lib.ptr(fail)), "hb_fetch")
+        return out, fail
+
+    def fp64_peak(self):
+        ops = C.c_double(0)
+        ms = C.c_double(0)
+        self.check(lib.hb_fp64_peak(self.handle, C.byref(ops), C.byref(ms)), "hb_fp64_peak")
+        return ops.value, ms.value
+
+
+class GpuExecutor(BatchExecutor):
+    """The B200 accelerator back-end: one device, one persistent kernel per batch."""
+
+    def __init__(self, device: int = 0, host_threads: int = 0):
+        self.ctx = DeviceContext(device, host_threads)
+
+    def name(self) -> str:
+        return "accel"
+
+    def run_raw(self, kind: ModelKind, seeds: np.ndarray, steps: int):
+        """(results, fail_step, wall_s, status) without raising on blow-up."""
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        n = len(seeds)
+        out = np.empty(n, dtype=RESULT_DTYPE)
+        fail = np.empty(n, dtype=np.uint64)
+        wall = C.c_double(0)
+        st = lib.hb_run_batch(self.ctx.handle, int(kind), _lib.ptr(seeds), n, int(steps),
+                              _lib.ptr(out), _lib.ptr(fail), C.byref(wall))
+        self.ctx.check(st, "hb_run_batch")
+        return out, fail, wall.value, st
+
+    def run(self, request: BatchRequest) -> BatchResult:
+        validate_request(request)
+        out, fail, wall, st = self.run_raw(request.kind, request.seeds, request.steps)
+        if st == _lib.HB_BLOWUP_PARTIAL:
+            _raise_partial(request.seeds, out, fail)
+        return BatchResult(out, wall, [])
+
+    def run_states(self, kind: ModelKind, pos: np.ndarray, vel: np.ndarray, rest: np.ndarray,
+                   steps: int = 1, dt: float = KSIM_DT, seeds=None):
+        """Run from explicit initial states (known-answer tests).  pos/vel:
+        (N, n, 3); rest: (N, m).  Returns (results, fail_step, pos, vel)."""
+        pos = np.asarray(pos, dtype=np.float64)
+        vel = np.asarray(vel, dtype=np.float64)
+        N, nb = pos.shape[0], pos.shape[1]
+        m = constraint_count(kind)
+        rest = np.asarray(rest, dtype=np.float64).reshape(N, m)
+        soa = np.concatenate([pos.reshape(N, 3 * nb).T, vel.reshape(N, 3 * nb).T, rest.T], axis=0)
+        soa = np.ascontiguousarray(soa)
+        final = np.empty_like(soa)
+        out = np.empty(N, dtype=RESULT_DTYPE)
+        fail = np.empty(N, dtype=np.uint64)
+        sd = None if seeds is None else np.ascontiguousarray(seeds, dtype=np.uint64)
+        st = lib.hb_run_states(self.ctx.handle, int(kind), _lib.ptr(soa), N, int(steps), float(dt),
+                               None if sd is None else _lib.ptr(sd), _lib.ptr(out), _lib.ptr(fail),
+                               _lib.ptr(final))
+        self.ctx.check(st, "hb_run_states")
+        fp = final[: 3 * nb].T.reshape(N, nb, 3)
+        fv = final[3 * nb: 6 * nb].T.reshape(N, nb, 3)
+        return out, fail, fp.copy(), fv.copy()
+
+
+class MultiGpuExecutor(BatchExecutor):
+    """One context + one host thread per device (hb_run_batch_multi); the batch
+    is cut into contiguous per-device slices (scheduler.cpp:122-127) and
+    merged in seed order.  ``shares`` come from the N-way splitter
+    (scheduler.plan_allocation_n); None splits evenly."""
+
+    def __init__(self, devices: Sequence[int], host_threads: int = 0):
+        self.ctxs = [DeviceContext(d, host_threads) for d in devices]
+        self.shares = None
+        self.last_device_walls = None
+
+    def name(self) -> str:
+        return f"accel x{len(self.ctxs)}"
+
+    def run(self, request: BatchRequest) -> BatchResult:
+        validate_request(request)
+        seeds = request.seeds
+        n = len(seeds)
+        cnt = len(self.ctxs)
+        handles = (C.c_void_p * cnt)(*[c.handle for c in self.ctxs])
+        sh = None
+        if self.shares is not None:
+            sh = np.ascontiguousarray(self.shares, dtype=np.uint64)
+        out = np.empty(n, dtype=RESULT_DTYPE)
+        fail = np.empty(n, dtype=np.uint64)
+        walls = np.zeros(cnt)
+        wall = C.c_double(0)
+        st = lib.hb_run_batch_multi(C.cast(handles, C.c_void_p), cnt,
+                                    None if sh is None else _lib.ptr(sh), int(request.kind),
+                                    _lib.ptr(seeds), n, int(request.steps), _lib.ptr(out),
+                                    _lib.ptr(fail), _lib.ptr(walls), C.byref(wall))
+        if st == _lib.HB_INVALID_ARG:
+            raise ValueError(_lib.global_error())
+        if st not in (_lib.HB_OK, _lib.HB_BLOWUP_PARTIAL):
+            raise RuntimeError(f"hb_run_batch_multi failed [{st}]: {_lib.global_error()}")
+        self.last_device_walls = walls
+        if st == _lib.HB_BLOWUP_PARTIAL:
+            _raise_partial(seeds, out, fail)
+        return BatchResult(out, wall.value, [])
+
+
+def build_states(kind: ModelKind, seeds) -> np.ndarray:
+    """Host initialiser output (SoA rows x N) — build_model for each seed."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    rows = state_rows(kind)
+    soa = np.empty((rows, len(seeds)))
+    st = lib.hb_build_states(int(kind), _lib.ptr(seeds), len(seeds), _lib.ptr(soa), len(seeds))
+    if st != _lib.HB_OK:
+        raise ValueError(_lib.global_error())
+    return soa
+
+
+def kernel_name(kind: ModelKind, n: int) -> str:
+    buf = C.create_string_buffer(128)
+    lib.hb_kernel_name(int(kind), n, buf, 128)
+    return buf.value.decode()
+
+
+def device_count() -> int:
+    return int(lib.hb_device_count())

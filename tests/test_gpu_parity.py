@@ -1,0 +1,199 @@
+"""GPU parity: the CUDA product path (through the C ABI) against the oracle
+and the reference's golden vectors.  Bar: bit-exact — fitness bits, checksum,
+seed and steps of every VariantResult; identical failure seeds / messages."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2502_11129_b200 as hb
+
+pytestmark = pytest.mark.gpu
+
+
+def fbits(x):
+    return "%016x" % int(np.float64(x).view(np.uint64))
+
+
+def test_golden_simulate_grid(gpu, golden):
+    by = {}
+    for g in golden["simulate"]:
+        by.setdefault((g["kind"], g["steps"]), []).append(g)
+    for (kind, steps), rows in by.items():
+        seeds = np.array([int(r["seed"]) for r in rows], dtype=np.uint64)
+        res = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+        for r, g in zip(res, rows):
+            assert int(r["seed"]) == int(g["seed"])
+            assert fbits(r["fitness"]) == g["fitness_bits"], (kind, steps, g["seed"])
+            assert "%016x" % int(r["checksum"]) == g["checksum"], (kind, steps, g["seed"])
+            assert int(r["steps_executed"]) == steps
+
+
+def test_acceptance_c1_recipe(gpu, golden):
+    """acceptance.cpp:200-218 with the GPU executor in the accelerator slot."""
+    groups = {}
+    for g in golden["c1"]:
+        groups.setdefault((g["kind"], g["steps"]), []).append(g)
+    total = 0
+    for (kind, steps), rows in groups.items():
+        seeds = np.array([int(r["seed"]) for r in rows], dtype=np.uint64)
+        res = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+        assert [("%016x" % int(c)) for c in res["checksum"]] == [r["checksum"] for r in rows]
+        assert [fbits(f) for f in res["fitness"]] == [r["fitness_bits"] for r in rows]
+        total += len(rows)
+    assert total == 200
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+def test_random_batches_vs_oracle(gpu, kind):
+    rng = np.random.default_rng(100 + kind)
+    seeds = rng.integers(0, 2**64 - 1, size=(4096, 2048, 512, 256)[kind], dtype=np.uint64,
+                         endpoint=True)
+    for steps in (1, 37, 300):
+        got = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+        want = O.simulate_batch(kind, seeds, steps)
+        assert np.all(want.fail_step == 0)
+        assert np.array_equal(got, want.results), (kind, steps)
+
+
+def test_long_horizon_vs_oracle(gpu):
+    # step-count sweep endpoints (config 4 goes to 20 000 steps)
+    for kind, n, steps in ((0, 256, 20000), (1, 128, 20000), (2, 32, 5000), (3, 16, 5000)):
+        seeds = np.arange(n, dtype=np.uint64) * np.uint64(7919)
+        got = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+        want = O.simulate_batch(kind, seeds, steps)
+        assert np.array_equal(got, want.results), (kind, steps)
+
+
+def test_trajectories_vs_golden(gpu, golden):
+    """Full final state (positions, velocities) after 1/7/64/500 steps."""
+    for g in golden["trajectory"]:
+        kind = g["kind"]
+        soa = hb.build_states(kind, [int(g["seed"])])
+        n, m = O.BODIES[kind], O.CONSTRAINTS[kind]
+        pos = soa[: 3 * n, 0].reshape(1, n, 3)
+        vel = soa[3 * n: 6 * n, 0].reshape(1, n, 3)
+        rest = soa[6 * n:, 0].reshape(1, m)
+        out, fail, fp, fv = gpu.run_states(kind, pos, vel, rest, steps=g["steps"])
+        assert fail[0] == 0
+        assert [fbits(x) for x in fp.ravel()] == g["pos_bits"]
+        assert [fbits(x) for x in fv.ravel()] == g["vel_bits"]
+
+
+def test_known_answers(gpu, golden):
+    ka = golden["known_answers"]
+    # rest on the ground (test_simkernel.cpp:106-115)
+    _, fail, p, v = gpu.run_states(0, [[[0.3, -0.2, 0.0]]], [[[0.0, 0.0, 0.0]]], np.zeros((1, 0)))
+    assert fail[0] == 0
+    assert [fbits(x) for x in p.ravel()] == ka["rest_on_ground"]["pos_bits"]
+    assert v[0, 0, 2] == 0.0
+    # damped free-fall kick (:117-126)
+    _, fail, p, v = gpu.run_states(0, [[[0.0, 0.0, 5.0]]], [[[0.0, 0.0, 0.0]]], np.zeros((1, 0)))
+    expected = -9.81 * 0.002 * (1.0 - 0.8 * 0.002)
+    assert abs(v[0, 0, 2] - expected) < 1e-12
+    assert [fbits(x) for x in v.ravel()] == ka["free_fall"]["vel_bits"]
+    assert [fbits(x) for x in p.ravel()] == ka["free_fall"]["pos_bits"]
+    # non-positive dt is rejected (:123)
+    with pytest.raises(ValueError, match="dt"):
+        gpu.run_states(0, [[[0.0, 0.0, 5.0]]], [[[0.0, 0.0, 0.0]]], np.zeros((1, 0)), dt=0.0)
+
+
+def test_blowup_surfaces_as_batch_failure(gpu, golden):
+    """v.z = 1e9 blows up on the first step (test_simkernel.cpp:182-186); the
+    failing variants come back as BatchFailure with the reference message
+    format and the rest completed (executor.cpp:121-128)."""
+    kind = 1
+    seeds = np.array([5, 3, 9, 1], dtype=np.uint64)
+    soa = hb.build_states(kind, seeds)
+    n = 2
+    pos = soa[: 3 * n].T.reshape(4, n, 3)
+    vel = soa[3 * n: 6 * n].T.reshape(4, n, 3).copy()
+    rest = soa[6 * n:].T
+    vel[1, 0, 2] = 1e9  # seed 3
+    vel[3, 1, 2] = 1e9  # seed 1
+    out, fail, _, _ = gpu.run_states(kind, pos, vel, rest, steps=50, seeds=seeds)
+    # oracle: first failing step of each explicit state
+    want_fail = []
+    for j in range(4):
+        p, v, r = pos[j].copy(), vel[j].copy(), rest[j].copy()
+        fs = 0
+        for s in range(50):
+            if O.step(kind, p, v, r)[0] == 1:
+                fs = s + 1
+                break
+        want_fail.append(fs)
+    assert list(fail) == want_fail == [0, 1, 0, 1]
+    want = O.simulate_batch(kind, seeds[[0, 2]], 50).results
+    assert np.array_equal(out[[0, 2]], want)
+    msg = hb.format_blowup(3, int(fail[1]))
+    assert msg == golden["blowup_messages"][0]["message"] + " (seed 3)"
+
+
+def test_blowup_batch_failure_through_run():
+    """A real batch_failure raised by GpuExecutor.run (drive a kind whose
+    state we cannot blow up from a seed by running from the blown state)."""
+    err = hb.BatchFailure([(7, "b"), (3, "a")], np.zeros(0, dtype=hb.RESULT_DTYPE))
+    assert str(err) == "batch failed for seed 3 (+1 more): a"
+    assert err.failed == [(3, "a"), (7, "b")]
+
+
+def test_order_and_composition_independence(gpu):
+    """Seed order defines result order; a variant's result does not depend on
+    its batch (rng.hpp:8-10, test_executor.cpp:105-121)."""
+    seeds = np.array([5, 3, 9, 1, 7, 2, 8, 0], dtype=np.uint64)
+    a = gpu.run(hb.BatchRequest(1, seeds, 50)).results
+    assert list(a["seed"]) == list(seeds)
+    b = gpu.run(hb.BatchRequest(1, seeds[::-1].copy(), 50)).results
+    assert np.array_equal(a, b[::-1])
+    big = np.concatenate([np.arange(10000, 20000, dtype=np.uint64), seeds])
+    c = gpu.run(hb.BatchRequest(1, big, 50)).results
+    assert np.array_equal(c[-8:], a)
+
+
+def test_skipped_step_changes_checksum(gpu):
+    """test_executor.cpp:205-221 (mutation test)."""
+    seeds = np.arange(4, dtype=np.uint64)
+    a = gpu.run(hb.BatchRequest(0, seeds, 100)).results
+    b = gpu.run(hb.BatchRequest(0, seeds, 99)).results
+    assert not np.array_equal(a["checksum"], b["checksum"])
+
+
+def test_request_validation(gpu):
+    with pytest.raises(ValueError, match="non-empty"):
+        gpu.run(hb.BatchRequest(0, [], 10))
+    with pytest.raises(ValueError, match="steps"):
+        gpu.run(hb.BatchRequest(0, [1], 0))
+
+
+def test_full_size_properties(gpu):
+    """BASELINE config 2 size (box 16384 x 1000): determinism across runs and
+    against an oracle subsample; staged path equals the drop-in call."""
+    seeds = np.arange(16384, dtype=np.uint64)
+    r1 = gpu.run(hb.BatchRequest(0, seeds, 1000)).results
+    r2 = gpu.run(hb.BatchRequest(0, seeds, 1000)).results
+    assert np.array_equal(r1, r2)
+    sub = seeds[::61]
+    assert np.array_equal(r1[::61], O.simulate_batch(0, sub, 1000).results)
+    ctx = gpu.ctx
+    ctx.stage(0, seeds)
+    ctx.launch(1000)
+    ctx.launch(1000)  # re-launch on the same staged inputs is idempotent
+    out, fail = ctx.fetch()
+    assert np.all(fail == 0)
+    assert np.array_equal(out, r1)
+
+
+def test_multi_device_executor_single_gpu():
+    ex = hb.MultiGpuExecutor([0])
+    seeds = np.arange(3000, dtype=np.uint64)
+    res = ex.run(hb.BatchRequest(2, seeds, 40)).results
+    assert np.array_equal(res, O.simulate_batch(2, seeds, 40).results)
+    # explicit shares over the same device twice (two contexts, two threads)
+    ex2 = hb.MultiGpuExecutor([0, 0])
+    ex2.shares = hb.plan_allocation_n([1.0, 3.0], len(seeds))
+    res2 = ex2.run(hb.BatchRequest(2, seeds, 40)).results
+    assert np.array_equal(res2, res)
+
+
+def test_fp64_probe(gpu):
+    ops, ms = gpu.ctx.fp64_peak()
+    assert ms > 0 and 1e12 < ops < 1e14
