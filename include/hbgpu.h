@@ -95,6 +95,15 @@ void* hb_ctx_stream(hb_ctx* ctx);
  * threads, capped at 64). 0 = default. */
 hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 
+/* Kernel family used by this context.  HB_KERNEL_AUTO (default) = the
+ * optimised kernels (branch-free projection with exact replay, two-lane
+ * humanoid, device-side Box init); HB_KERNEL_GENERIC = the plain
+ * reference-order kernel (library sqrt / '/', every branch), kept as an
+ * in-tree cross-check.  Both are bit-exact with simulate(). */
+#define HB_KERNEL_AUTO 0
+#define HB_KERNEL_GENERIC 1
+hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
+
 /* ---- the drop-in call ------------------------------------------------------
  * batch_executor::run (executor.hpp:70) for `n` seeds through `steps` fixed
  * dt = kSimDt steps.  out[i] is the VariantResult of seeds[i] (seed order);
@@ -167,6 +176,15 @@ hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* sha
  * Times a dependent-chain-free DADD/DMUL stream on the context's device and
  * returns the sustained non-FMA FP64 op rate (ops/s) and the kernel time. */
 hb_status hb_fp64_peak(hb_ctx* ctx, double* ops_per_s, double* ms);
+
+/* ---- fast-path self test ----------------------------------------------------
+ * Evaluates the kernels' branch-free sqrt(x[i]) and x[i] / y[i] replicas and
+ * the library IEEE versions on the device.  Counts operands where the replica
+ * claims validity but differs in any bit (must be 0), and operands the
+ * replica flags for exact replay. */
+hb_status hb_check_fast_math(hb_ctx* ctx, const double* x, const double* y, size_t n,
+                             uint64_t* sqrt_mismatch, uint64_t* div_mismatch,
+                             uint64_t* sqrt_flagged, uint64_t* div_flagged);
 
 #ifdef __cplusplus
 }

@@ -10,22 +10,30 @@
 
 namespace hb {
 
-// One batch on one device.  init: SoA rows (state_rows(kind) x ld doubles),
-// read-only.  out / fail: n entries.  final_state (nullable): SoA rows.
+// One batch on one device.
+//  init:  SoA rows (state_rows(kind) x ld doubles), read-only; nullptr for
+//         Box means "generate the initial state from seeds on the device".
+//  seeds: device seeds (n).
+//  fc:    n x {fitness, checksum bits} (16 B per variant).
+//  fail:  n x first failing step (0 = completed); fail_count += #failed.
+//  final_state (nullable): SoA rows, ld.
 struct SimArgs {
     const double* init;
+    const uint64_t* seeds;
     size_t n;
     size_t ld;
     uint64_t steps;
     double dt;
-    const uint64_t* seeds;  // device pointer, nullable
-    hb_variant_result* out;
+    double2* fc;
     uint64_t* fail;
+    unsigned* fail_count;
     double* final_state;
 };
 
-cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms);
-const char* kernel_name(int kind, size_t n);
+cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);
+const char* kernel_name(int kind, size_t n, int variant);
 cudaError_t launch_fp64_probe(double* scratch, int sms, int iters, cudaStream_t st, double* ops);
+cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, double* o0, double* o1,
+                                  double* o2, double* o3, unsigned char* flags, cudaStream_t st);
 
 }  // namespace hb

@@ -43,43 +43,49 @@ bool valid_kind(int kind) { return kind >= 0 && kind <= 3; }
 
 // ---------------------------------------------------------------------------
 // Persistent fork/join pool.  The caller thread takes part; work is handed
-// out in contiguous chunks (like cpu_executor, executor.cpp:93-113).
+// out in contiguous chunks (like cpu_executor, executor.cpp:93-113).  Idle
+// workers spin for a short while before sleeping so that back-to-back
+// batches do not pay a futex wake-up per call.
 class ThreadPool {
 public:
     explicit ThreadPool(int threads) : n_(std::max(1, threads)) {
-        for (int t = 1; t < n_; ++t) workers_.emplace_back([this, t] { loop(t); });
+        for (int t = 1; t < n_; ++t) workers_.emplace_back([this] { loop(); });
     }
     ~ThreadPool() {
         {
             std::lock_guard<std::mutex> g(m_);
-            stop_ = true;
-            ++gen_;
+            stop_.store(true);
+            gen_.fetch_add(1);
         }
         cv_.notify_all();
         for (auto& w : workers_) w.join();
     }
     int size() const { return n_; }
 
-    // fn(begin, end) over [0, total) split into `parts` contiguous chunks.
-    void run(size_t total, const std::function<void(size_t, size_t)>& fn) {
+    // fn(begin, end) over [0, total) in up to `n_` contiguous chunks of at
+    // least `grain` items.
+    void run(size_t total, const std::function<void(size_t, size_t)>& fn, size_t grain = 1) {
         if (total == 0) return;
-        const int parts = static_cast<int>(std::min<size_t>(n_, total));
+        const size_t max_parts = std::max<size_t>(1, total / std::max<size_t>(1, grain));
+        const int parts = static_cast<int>(std::min<size_t>(n_, max_parts));
         if (parts == 1) {
             fn(0, total);
             return;
         }
-        std::unique_lock<std::mutex> lk(m_);
-        fn_ = &fn;
-        total_ = total;
-        parts_ = parts;
-        next_.store(0);
-        done_ = 0;
-        ++gen_;
-        lk.unlock();
+        {
+            std::lock_guard<std::mutex> g(m_);
+            fn_ = &fn;
+            total_ = total;
+            parts_ = parts;
+            next_.store(0);
+            done_.store(0);
+            gen_.fetch_add(1);
+        }
         cv_.notify_all();
         work();
-        lk.lock();
-        done_cv_.wait(lk, [&] { return done_ == parts_; });
+        while (done_.load(std::memory_order_acquire) != parts_) {
+        }
+        std::lock_guard<std::mutex> g(m_);
         fn_ = nullptr;
     }
 
@@ -92,17 +98,24 @@ private:
             const size_t b = part * chunk + std::min<size_t>(part, extra);
             const size_t e = b + chunk + (static_cast<size_t>(part) < extra ? 1 : 0);
             (*fn_)(b, e);
-            std::lock_guard<std::mutex> g(m_);
-            if (++done_ == parts_) done_cv_.notify_all();
+            done_.fetch_add(1, std::memory_order_release);
         }
     }
-    void loop(int) {
-        uint64_t seen = 0;
+    void loop() {
+        uint64_t seen = gen_.load();
         for (;;) {
+            // spin ~100 us, then sleep on the condition variable
+            auto t0 = std::chrono::steady_clock::now();
+            while (gen_.load(std::memory_order_acquire) == seen) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(100)) {
+                    std::unique_lock<std::mutex> lk(m_);
+                    cv_.wait(lk, [&] { return gen_.load() != seen; });
+                    break;
+                }
+            }
+            seen = gen_.load();
+            if (stop_.load()) return;
             std::unique_lock<std::mutex> lk(m_);
-            cv_.wait(lk, [&] { return gen_ != seen; });
-            seen = gen_;
-            if (stop_) return;
             if (!fn_) continue;
             lk.unlock();
             work();
@@ -111,14 +124,14 @@ private:
     int n_;
     std::vector<std::thread> workers_;
     std::mutex m_;
-    std::condition_variable cv_, done_cv_;
+    std::condition_variable cv_;
     const std::function<void(size_t, size_t)>* fn_ = nullptr;
     size_t total_ = 0;
     int parts_ = 0;
     std::atomic<int> next_{0};
-    int done_ = 0;
-    uint64_t gen_ = 0;
-    bool stop_ = false;
+    std::atomic<int> done_{0};
+    std::atomic<uint64_t> gen_{0};
+    std::atomic<bool> stop_{false};
 };
 
 int default_host_threads() {
@@ -184,6 +197,12 @@ void build_range(int kind, const uint64_t* seeds, size_t b, size_t e, double* so
     }
 }
 
+inline long long __double_as_longlong_host(double x) {
+    long long v;
+    std::memcpy(&v, &x, sizeof v);
+    return v;
+}
+
 double elapsed_s(std::chrono::steady_clock::time_point t0) {
     return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
@@ -194,6 +213,7 @@ double elapsed_s(std::chrono::steady_clock::time_point t0) {
 struct hb_ctx {
     int device = 0;
     int sms = 148;
+    int kernel_variant = HB_KERNEL_AUTO;
     cudaStream_t stream = nullptr;
     std::string err;
     ThreadPool* pool = nullptr;
@@ -203,9 +223,10 @@ struct hb_ctx {
     double* d_init = nullptr;
     size_t d_init_cap = 0;  // doubles
     uint64_t* d_seeds = nullptr;
-    hb_variant_result* d_out = nullptr;
+    double2* d_fc = nullptr;   // {fitness, checksum bits} per variant
     uint64_t* d_fail = nullptr;
     size_t d_n_cap = 0;
+    unsigned* d_count = nullptr;  // failed-variant counter
     double* d_final = nullptr;
     size_t d_final_cap = 0;
     double* d_scratch = nullptr;
@@ -214,13 +235,16 @@ struct hb_ctx {
     double* h_init = nullptr;
     size_t h_init_cap = 0;
     uint64_t* h_seeds = nullptr;
-    hb_variant_result* h_out = nullptr;
+    double2* h_fc = nullptr;
     uint64_t* h_fail = nullptr;
     size_t h_n_cap = 0;
+    unsigned* h_count = nullptr;
 
-    // staged batch
+    // the batch currently resident on the device
     int staged_kind = -1;
     size_t staged_n = 0;
+    bool staged_from_seeds = false;
+    uint64_t last_steps = 0;
 
     hb_status fail(hb_status st, const std::string& msg) {
         err = msg;
@@ -241,40 +265,46 @@ namespace {
         if (_st != HB_OK) return _st;         \
     } while (0)
 
-hb_status ensure_capacity(hb_ctx* c, int kind, size_t n) {
-    const size_t rows = static_cast<size_t>(hb::state_rows(kind));
-    const size_t need = rows * n;
+template <class T>
+hb_status grow_dev(hb_ctx* c, T** p, size_t& cap, size_t need, const char* what) {
+    if (need <= cap) return HB_OK;
+    if (*p) cudaFree(*p);
+    *p = nullptr;
+    const size_t nc = std::max(need, cap * 2);
+    HB_TRY(c->cuda(cudaMalloc(reinterpret_cast<void**>(p), nc * sizeof(T)), what));
+    cap = nc;
+    return HB_OK;
+}
+
+hb_status ensure_capacity(hb_ctx* c, int kind, size_t n, bool need_init) {
     HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
-    if (need > c->d_init_cap) {
-        if (c->d_init) cudaFree(c->d_init);
-        c->d_init = nullptr;
-        const size_t cap = std::max(need, c->d_init_cap * 2);
-        HB_TRY(c->cuda(cudaMalloc(&c->d_init, cap * sizeof(double)), "cudaMalloc(init)"));
-        c->d_init_cap = cap;
-    }
-    if (need > c->h_init_cap) {
-        if (c->h_init) cudaFreeHost(c->h_init);
-        c->h_init = nullptr;
-        const size_t cap = std::max(need, c->h_init_cap * 2);
-        HB_TRY(c->cuda(cudaHostAlloc(&c->h_init, cap * sizeof(double), cudaHostAllocPortable),
-                       "cudaHostAlloc(init)"));
-        c->h_init_cap = cap;
+    if (need_init) {
+        const size_t need = static_cast<size_t>(hb::state_rows(kind)) * n;
+        HB_TRY(grow_dev(c, &c->d_init, c->d_init_cap, need, "cudaMalloc(init)"));
+        if (need > c->h_init_cap) {
+            if (c->h_init) cudaFreeHost(c->h_init);
+            c->h_init = nullptr;
+            const size_t cap = std::max(need, c->h_init_cap * 2);
+            HB_TRY(c->cuda(cudaHostAlloc(&c->h_init, cap * sizeof(double), cudaHostAllocPortable),
+                           "cudaHostAlloc(init)"));
+            c->h_init_cap = cap;
+        }
     }
     if (n > c->d_n_cap) {
-        cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
-        c->d_seeds = nullptr; c->d_out = nullptr; c->d_fail = nullptr;
+        cudaFree(c->d_seeds); cudaFree(c->d_fc); cudaFree(c->d_fail);
+        c->d_seeds = nullptr; c->d_fc = nullptr; c->d_fail = nullptr;
         const size_t cap = std::max(n, c->d_n_cap * 2);
         HB_TRY(c->cuda(cudaMalloc(&c->d_seeds, cap * sizeof(uint64_t)), "cudaMalloc(seeds)"));
-        HB_TRY(c->cuda(cudaMalloc(&c->d_out, cap * sizeof(hb_variant_result)), "cudaMalloc(out)"));
+        HB_TRY(c->cuda(cudaMalloc(&c->d_fc, cap * sizeof(double2)), "cudaMalloc(fc)"));
         HB_TRY(c->cuda(cudaMalloc(&c->d_fail, cap * sizeof(uint64_t)), "cudaMalloc(fail)"));
         c->d_n_cap = cap;
     }
     if (n > c->h_n_cap) {
-        cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
-        c->h_seeds = nullptr; c->h_out = nullptr; c->h_fail = nullptr;
+        cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_fc); cudaFreeHost(c->h_fail);
+        c->h_seeds = nullptr; c->h_fc = nullptr; c->h_fail = nullptr;
         const size_t cap = std::max(n, c->h_n_cap * 2);
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_seeds, cap * sizeof(uint64_t), 0), "cudaHostAlloc(seeds)"));
-        HB_TRY(c->cuda(cudaHostAlloc(&c->h_out, cap * sizeof(hb_variant_result), 0), "cudaHostAlloc(out)"));
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_fc, cap * sizeof(double2), 0), "cudaHostAlloc(fc)"));
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_fail, cap * sizeof(uint64_t), 0), "cudaHostAlloc(fail)"));
         c->h_n_cap = cap;
     }
@@ -295,35 +325,85 @@ hb_status validate(hb_ctx* c, int kind, const void* seeds, size_t n, uint64_t st
     return HB_OK;
 }
 
-// Host init of `n` seeds into the pinned SoA image + async H2D of state and seeds.
+// Box in the optimised family builds its initial state on the device from
+// the seed; every other model gets the host initialiser (glibc cos / sin).
+bool init_on_device(const hb_ctx* c, int kind) {
+    return kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO;
+}
+
+constexpr size_t kParallelCopyMin = 1 << 15;  // items below which one thread copies
+
+// Seeds (+ host-built initial states) into pinned memory, async H2D.
 hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
-    HB_TRY(ensure_capacity(c, kind, n));
-    std::memcpy(c->h_seeds, seeds, n * sizeof(uint64_t));
-    double* soa = c->h_init;
-    pool_of(c).run(n, [&](size_t b, size_t e) { build_range(kind, seeds, b, e, soa, n); });
-    const size_t rows = static_cast<size_t>(hb::state_rows(kind));
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
-                                   cudaMemcpyHostToDevice, c->stream), "H2D init"));
+    const bool dev_init = init_on_device(c, kind);
+    HB_TRY(ensure_capacity(c, kind, n, !dev_init));
+    uint64_t* hs = c->h_seeds;
+    if (dev_init) {
+        pool_of(c).run(n, [&](size_t b, size_t e) {
+            std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
+        }, kParallelCopyMin);
+    } else {
+        double* soa = c->h_init;
+        pool_of(c).run(n, [&](size_t b, size_t e) {
+            std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
+            build_range(kind, seeds, b, e, soa, n);
+        }, 64);
+        const size_t rows = static_cast<size_t>(hb::state_rows(kind));
+        HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
+                                       cudaMemcpyHostToDevice, c->stream), "H2D init"));
+    }
     HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, c->h_seeds, n * sizeof(uint64_t),
                                    cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+    c->staged_kind = kind;
+    c->staged_n = n;
+    c->staged_from_seeds = dev_init;
     return HB_OK;
 }
 
-hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, double* d_final) {
-    hb::SimArgs a{c->d_init, n, n, steps, dt, c->d_seeds, c->d_out, c->d_fail, d_final};
-    return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms), "kernel launch");
+hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool from_seeds,
+                 double* d_final) {
+    HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned), c->stream), "memset(count)"));
+    hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
+                  c->d_fc, c->d_fail, c->d_count, d_final};
+    c->last_steps = steps;
+    return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch");
 }
 
-hb_status fetch(hb_ctx* c, size_t n, hb_variant_result* out, uint64_t* fail_step, bool* any_fail) {
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_out, c->d_out, n * sizeof(hb_variant_result),
-                                   cudaMemcpyDeviceToHost, c->stream), "D2H results"));
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_fail, c->d_fail, n * sizeof(uint64_t),
-                                   cudaMemcpyDeviceToHost, c->stream), "D2H status"));
+// D2H of the compact records + failure count; assemble 32-byte
+// VariantResults (seed and steps are known on the host) in seed order.
+hb_status fetch(hb_ctx* c, size_t n, const uint64_t* seeds, uint64_t steps, hb_variant_result* out,
+                uint64_t* fail_step, bool* any_fail) {
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_fc, c->d_fc, n * sizeof(double2), cudaMemcpyDeviceToHost,
+                                   c->stream), "D2H results"));
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                   c->stream), "D2H count"));
     HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
-    std::memcpy(out, c->h_out, n * sizeof(hb_variant_result));
-    bool any = false;
-    for (size_t i = 0; i < n; ++i) any |= (c->h_fail[i] != 0);
-    if (fail_step) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
+    const bool any = *c->h_count != 0;
+    if (any) {
+        HB_TRY(c->cuda(cudaMemcpy(c->h_fail, c->d_fail, n * sizeof(uint64_t), cudaMemcpyDeviceToHost),
+                       "D2H fail"));
+    }
+    const double2* fc = c->h_fc;
+    const uint64_t* hf = c->h_fail;
+    pool_of(c).run(n, [&](size_t b, size_t e) {
+        for (size_t i = b; i < e; ++i) {
+            hb_variant_result r;
+            r.seed = seeds[i];
+            r.fitness = fc[i].x;
+            r.checksum = static_cast<uint64_t>(__double_as_longlong_host(fc[i].y));
+            r.steps_executed = steps;
+            if (any && hf[i]) {
+                r.fitness = 0.0;
+                r.checksum = 0;
+                r.steps_executed = hf[i];
+            }
+            out[i] = r;
+        }
+        if (fail_step) {
+            if (any) std::memcpy(fail_step + b, hf + b, (e - b) * sizeof(uint64_t));
+            else std::memset(fail_step + b, 0, (e - b) * sizeof(uint64_t));
+        }
+    }, kParallelCopyMin);
     *any_fail = any;
     return HB_OK;
 }
@@ -373,7 +453,9 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
     c->sms = prop.multiProcessorCount;
     if (cudaSetDevice(device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaMalloc(&c->d_scratch, 64) != cudaSuccess) {
+        cudaMalloc(&c->d_scratch, 64) != cudaSuccess ||
+        cudaMalloc(&c->d_count, 16) != cudaSuccess ||
+        cudaHostAlloc(&c->h_count, 16, 0) != cudaSuccess) {
         delete c;
         return set_global(HB_CUDA_ERROR, "stream/scratch creation failed");
     }
@@ -385,9 +467,10 @@ void hb_ctx_destroy(hb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
-    cudaFree(c->d_final); cudaFree(c->d_scratch);
-    cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
+    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_fc); cudaFree(c->d_fail);
+    cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count);
+    cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_fc); cudaFreeHost(c->h_fail);
+    cudaFreeHost(c->h_count);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c->pool;
     delete c;
@@ -405,6 +488,14 @@ hb_status hb_ctx_set_host_threads(hb_ctx* c, int threads) {
     return HB_OK;
 }
 
+hb_status hb_ctx_set_kernel(hb_ctx* c, int variant) {
+    if (!c || (variant != HB_KERNEL_AUTO && variant != HB_KERNEL_GENERIC))
+        return set_global(HB_INVALID_ARG, "bad kernel variant");
+    c->kernel_variant = variant;
+    c->staged_kind = -1;
+    return HB_OK;
+}
+
 hb_status hb_build_states(int kind, const uint64_t* seeds, size_t n, double* soa, size_t ld) {
     if (!valid_kind(kind)) return set_global(HB_INVALID_ARG, "unknown model kind");
     if (!seeds || !soa || ld < n) return set_global(HB_INVALID_ARG, "bad buffers");
@@ -417,10 +508,9 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
     const auto t0 = std::chrono::steady_clock::now();
     HB_TRY(validate(c, kind, seeds, n, steps, out));
     HB_TRY(stage_inputs(c, kind, seeds, n));
-    HB_TRY(launch(c, kind, n, steps, hb::kSimDt, nullptr));
-    c->staged_kind = -1;  // d_init now holds this batch; not a staged launch target
+    HB_TRY(launch(c, kind, n, steps, hb::kSimDt, c->staged_from_seeds, nullptr));
     bool any = false;
-    HB_TRY(fetch(c, n, out, fail_step, &any));
+    HB_TRY(fetch(c, n, seeds, steps, out, fail_step, &any));
     if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
     return HB_OK;
@@ -434,26 +524,23 @@ hb_status hb_run_states(hb_ctx* c, int kind, const double* init_soa, size_t n, u
     if (!init_soa || !out || n == 0) return c->fail(HB_INVALID_ARG, "bad buffers");
     if (steps < 1) return c->fail(HB_INVALID_ARG, "simulate: steps must be >= 1");
     if (!(dt > 0.0)) return c->fail(HB_INVALID_ARG, "step: dt must be > 0");
-    HB_TRY(ensure_capacity(c, kind, n));
+    HB_TRY(ensure_capacity(c, kind, n, true));
     const size_t rows = static_cast<size_t>(hb::state_rows(kind));
     const size_t bytes = rows * n * sizeof(double);
-    if (final_soa && rows * n > c->d_final_cap) {
-        cudaFree(c->d_final);
-        c->d_final = nullptr;
-        HB_TRY(c->cuda(cudaMalloc(&c->d_final, bytes), "cudaMalloc(final)"));
-        c->d_final_cap = rows * n;
-    }
+    if (final_soa) HB_TRY(grow_dev(c, &c->d_final, c->d_final_cap, rows * n, "cudaMalloc(final)"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, init_soa, bytes, cudaMemcpyHostToDevice, c->stream), "H2D"));
-    if (seeds) {
-        HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, seeds, n * sizeof(uint64_t),
-                                       cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
-    } else {
-        HB_TRY(c->cuda(cudaMemsetAsync(c->d_seeds, 0, n * sizeof(uint64_t), c->stream), "memset"));
+    std::vector<uint64_t> zeros;
+    const uint64_t* sd = seeds;
+    if (!sd) {
+        zeros.assign(n, 0);
+        sd = zeros.data();
     }
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, sd, n * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                   c->stream), "H2D seeds"));
     c->staged_kind = -1;
-    HB_TRY(launch(c, kind, n, steps, dt, final_soa ? c->d_final : nullptr));
+    HB_TRY(launch(c, kind, n, steps, dt, false, final_soa ? c->d_final : nullptr));
     bool any = false;
-    HB_TRY(fetch(c, n, out, fail_step, &any));
+    HB_TRY(fetch(c, n, sd, steps, out, fail_step, &any));
     if (final_soa) {
         HB_TRY(c->cuda(cudaMemcpy(final_soa, c->d_final, bytes, cudaMemcpyDeviceToHost), "D2H final"));
     }
@@ -464,10 +551,7 @@ hb_status hb_run_states(hb_ctx* c, int kind, const double* init_soa, size_t n, u
 hb_status hb_stage(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
     HB_TRY(validate(c, kind, seeds, n, 1, seeds));
     HB_TRY(stage_inputs(c, kind, seeds, n));
-    HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
-    c->staged_kind = kind;
-    c->staged_n = n;
-    return HB_OK;
+    return c->cuda(cudaStreamSynchronize(c->stream), "stream sync");
 }
 
 hb_status hb_launch(hb_ctx* c, uint64_t steps) {
@@ -475,7 +559,7 @@ hb_status hb_launch(hb_ctx* c, uint64_t steps) {
     if (c->staged_kind < 0) return c->fail(HB_INVALID_ARG, "hb_launch: no staged batch");
     if (steps < 1) return c->fail(HB_INVALID_ARG, "batch request: steps must be >= 1");
     HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
-    return launch(c, c->staged_kind, c->staged_n, steps, hb::kSimDt, nullptr);
+    return launch(c, c->staged_kind, c->staged_n, steps, hb::kSimDt, c->staged_from_seeds, nullptr);
 }
 
 hb_status hb_synchronize(hb_ctx* c) {
@@ -487,14 +571,14 @@ hb_status hb_fetch(hb_ctx* c, hb_variant_result* out, uint64_t* fail_step) {
     if (!c || !out) return set_global(HB_INVALID_ARG, "bad arguments");
     if (c->staged_kind < 0) return c->fail(HB_INVALID_ARG, "hb_fetch: no staged batch");
     bool any = false;
-    HB_TRY(fetch(c, c->staged_n, out, fail_step, &any));
+    HB_TRY(fetch(c, c->staged_n, c->h_seeds, c->last_steps, out, fail_step, &any));
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
     return HB_OK;
 }
 
 hb_status hb_kernel_name(int kind, size_t n, char* buf, size_t cap) {
     if (!valid_kind(kind) || !buf || cap == 0) return set_global(HB_INVALID_ARG, "bad arguments");
-    std::snprintf(buf, cap, "%s", hb::kernel_name(kind, n));
+    std::snprintf(buf, cap, "%s", hb::kernel_name(kind, n, HB_KERNEL_AUTO));
     return HB_OK;
 }
 
@@ -638,6 +722,46 @@ hb_status hb_fp64_peak(hb_ctx* c, double* ops_per_s, double* ms) {
     cudaEventDestroy(e1);
     *ops_per_s = ops / (static_cast<double>(t) * 1e-3);
     if (ms) *ms = t;
+    return HB_OK;
+}
+
+
+hb_status hb_check_fast_math(hb_ctx* c, const double* x, const double* y, size_t n,
+                             uint64_t* sqrt_mismatch, uint64_t* div_mismatch,
+                             uint64_t* sqrt_flagged, uint64_t* div_flagged) {
+    if (!c || !x || !y || n == 0) return set_global(HB_INVALID_ARG, "bad arguments");
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    double* d = nullptr;
+    unsigned char* fl = nullptr;
+    HB_TRY(c->cuda(cudaMalloc(&d, 6 * n * sizeof(double)), "cudaMalloc"));
+    if (cudaMalloc(&fl, n) != cudaSuccess) {
+        cudaFree(d);
+        return c->fail(HB_CUDA_ERROR, "cudaMalloc(flags)");
+    }
+    std::vector<double> o(4 * n);
+    std::vector<unsigned char> f(n);
+    cudaMemcpy(d, x, n * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemcpy(d + n, y, n * sizeof(double), cudaMemcpyHostToDevice);
+    cudaError_t e = hb::launch_fastpath_check(d, d + n, n, d + 2 * n, d + 3 * n, d + 4 * n, d + 5 * n,
+                                              fl, c->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(o.data(), d + 2 * n, 4 * n * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(f.data(), fl, n, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    cudaFree(fl);
+    HB_TRY(c->cuda(e, "fast-math check"));
+    uint64_t sm = 0, dm = 0, sf = 0, df = 0;
+    for (size_t i = 0; i < n; ++i) {
+        const bool fs = f[i] & 1, fd = f[i] & 2;
+        sf += fs;
+        df += fd;
+        if (!fs && std::memcmp(&o[i], &o[n + i], 8) != 0) ++sm;
+        if (!fd && std::memcmp(&o[2 * n + i], &o[3 * n + i], 8) != 0) ++dm;
+    }
+    if (sqrt_mismatch) *sqrt_mismatch = sm;
+    if (div_mismatch) *div_mismatch = dm;
+    if (sqrt_flagged) *sqrt_flagged = sf;
+    if (div_flagged) *div_flagged = df;
     return HB_OK;
 }
 

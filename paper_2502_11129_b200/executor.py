@@ -185,6 +185,20 @@ class DeviceContext:
         self.check(lib.hb_fetch(self.handle, _lib.ptr(out), _lib.ptr(fail)), "hb_fetch")
         return out, fail
 
+    def set_kernel(self, variant: int) -> None:
+        """_lib.HB_KERNEL_AUTO (optimised) or _lib.HB_KERNEL_GENERIC (reference-order cross-check)."""
+        self.check(lib.hb_ctx_set_kernel(self.handle, int(variant)), "hb_ctx_set_kernel")
+
+    def check_fast_math(self, x: np.ndarray, y: np.ndarray):
+        """(sqrt_mismatch, div_mismatch, sqrt_flagged, div_flagged) of the
+        kernels' branch-free sqrt / div replicas against the library on the device."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        r = [C.c_uint64(0) for _ in range(4)]
+        self.check(lib.hb_check_fast_math(self.handle, _lib.ptr(x), _lib.ptr(y), len(x),
+                                          *[C.byref(v) for v in r]), "hb_check_fast_math")
+        return tuple(int(v.value) for v in r)
+
     def fp64_peak(self):
         ops = C.c_double(0)
         ms = C.c_double(0)
@@ -195,8 +209,10 @@ class DeviceContext:
 class GpuExecutor(BatchExecutor):
     """The B200 accelerator back-end: one device, one persistent kernel per batch."""
 
-    def __init__(self, device: int = 0, host_threads: int = 0):
+    def __init__(self, device: int = 0, host_threads: int = 0, kernel: int = _lib.HB_KERNEL_AUTO):
         self.ctx = DeviceContext(device, host_threads)
+        if kernel != _lib.HB_KERNEL_AUTO:
+            self.ctx.set_kernel(kernel)
 
     def name(self) -> str:
         return "accel"

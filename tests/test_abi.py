@@ -164,3 +164,32 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "hb_oracle" not in src and "libhetbench_ref" not in src, f
+
+
+def test_box_device_init_sign_rule_matches_libm():
+    """The Box kernel derives sign(cos(a)) / sign(sin(a)) of the heading from
+    RN(pi/2) < a <= RN(3pi/2) and a > RN(pi) (hb_kernels.cu box_init); check the
+    rule against glibc at and around every boundary and on random headings."""
+    import ctypes.util
+    libm = C.CDLL(ctypes.util.find_library("m"))
+    libm.cos.restype = libm.sin.restype = C.c_double
+    libm.cos.argtypes = libm.sin.argtypes = [C.c_double]
+
+    def rule(a):
+        cneg = 1.5707963267948966 < a <= 4.71238898038469
+        sneg = a > 3.141592653589793
+        return cneg, sneg
+
+    pts = [0.0, 6.283185307179586]
+    for b in (1.5707963267948966, 3.141592653589793, 4.71238898038469):
+        x = b
+        for _ in range(5):
+            x = np.nextafter(x, -np.inf)
+        for _ in range(11):
+            pts.append(float(x))
+            x = np.nextafter(x, np.inf)
+    rng = np.random.default_rng(0)
+    pts += list(rng.uniform(0, 6.283185307179586, 20000))
+    for a in pts:
+        c, s = libm.cos(a), libm.sin(a)
+        assert rule(a) == (np.signbit(c), np.signbit(s)), a

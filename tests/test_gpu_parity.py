@@ -197,3 +197,68 @@ def test_multi_device_executor_single_gpu():
 def test_fp64_probe(gpu):
     ops, ms = gpu.ctx.fp64_peak()
     assert ms > 0 and 1e12 < ops < 1e14
+
+
+@pytest.fixture(scope="module")
+def gpu_generic():
+    ex = hb.GpuExecutor(0, kernel=1)
+    yield ex
+    ex.ctx.close()
+
+
+@pytest.mark.parametrize("kind,n,steps", [(0, 200000, 300), (1, 65536, 200), (2, 16384, 100),
+                                          (3, 8192, 40)])
+def test_optimised_equals_generic_kernel(gpu, gpu_generic, kind, n, steps):
+    """The optimised kernels (device-side Box init, branch-free projection with
+    exact replay, two-lane humanoid) against the plain reference-order kernel
+    (host init, library sqrt / '/') on large random batches, bit for bit."""
+    rng = np.random.default_rng(7 + kind)
+    seeds = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+    a = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+    b = gpu_generic.run(hb.BatchRequest(kind, seeds, steps)).results
+    assert np.array_equal(a, b)
+
+
+def test_fast_math_replicas(gpu):
+    """Branch-free sqrt / div replicas are bit-identical to the library
+    wherever they claim validity; out-of-range operands are flagged."""
+    rng = np.random.default_rng(11)
+    n = 1 << 22
+    # the operand ranges the projection sees: squared distances and corrections
+    x = np.concatenate([rng.uniform(1e-6, 10.0, n // 4), 10.0 ** rng.uniform(-30, 30, n // 4),
+                        rng.uniform(-1e-3, 1e-3, n // 4) * 0.5,
+                        np.frombuffer(rng.bytes(8 * (n // 4)), dtype=np.float64)])
+    y = np.concatenate([rng.uniform(1e-3, 3.0, n // 4), 10.0 ** rng.uniform(-12, 12, n // 4),
+                        rng.uniform(0.01, 2.0, n // 4),
+                        np.frombuffer(rng.bytes(8 * (n // 4)), dtype=np.float64)])
+    x[:16] = [0.0, -0.0, 1e-320, np.inf, np.nan, 1.0, 4.0, 2.0, 1e300, 1e-300, 5e-324,
+              2.2250738585072014e-308, 1.7976931348623157e308, 0.25, 9.0, 1e-24]
+    sm, dm, sf, df = gpu.ctx.check_fast_math(np.abs(x), y)
+    assert sm == 0 and dm == 0
+    # realistic operands are essentially never flagged
+    sm2, dm2, sf2, df2 = gpu.ctx.check_fast_math(x[: n // 4], y[: n // 4])
+    assert (sm2, dm2) == (0, 0) and sf2 == 0 and df2 <= 1
+    # signed x (division numerators can be negative)
+    sm3, dm3, _, _ = gpu.ctx.check_fast_math(x[n // 2: 3 * n // 4], y[n // 2: 3 * n // 4])
+    assert dm3 == 0
+
+
+def test_exact_replay_path_blowup_states(gpu, gpu_generic):
+    """States that hit the replay path (huge / degenerate coordinates) agree
+    with the generic kernel (fail step and surviving results)."""
+    kind = 2
+    seeds = np.arange(64, dtype=np.uint64)
+    soa = hb.build_states(kind, seeds)
+    n = 12
+    pos = soa[: 3 * n].T.reshape(64, n, 3).copy()
+    vel = soa[3 * n: 6 * n].T.reshape(64, n, 3).copy()
+    rest = soa[6 * n:].T.copy()
+    vel[::3, 5, 2] = 1e5       # violent but finite
+    vel[1::7, 0, :] = 3e5
+    pos[2::5, 3, :] = pos[2::5, 4, :]   # coincident bodies -> dist < 1e-12 path
+    a = gpu.run_states(kind, pos, vel, rest, steps=30, seeds=seeds)
+    b = gpu_generic.run_states(kind, pos, vel, rest, steps=30, seeds=seeds)
+    assert np.array_equal(a[1], b[1])
+    ok = a[1] == 0
+    assert np.array_equal(a[0][ok], b[0][ok])
+    assert np.array_equal(a[2][ok], b[2][ok]) and np.array_equal(a[3][ok], b[3][ok])
