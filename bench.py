@@ -277,6 +277,7 @@ def run_ours(a, ws, rank, local):
     value = units / (ms_per_step * 1e-3)
     out, fail = ctx.fetch()
     assert int(np.sum(fail)) == 0, "blow-up in bench workload"
+    _, replays = ctx.last_launch_stats()
 
     # ---- roofline: FP64 pipe (measured probe on this device) ----
     peak_ops, _ = ctx.fp64_peak()
@@ -290,6 +291,7 @@ def run_ours(a, ws, rank, local):
                            "MEASURED_PEAKS.json has no FP64 figure",
             "kernel": hb.kernel_name(kind, n),
             "kernel_ms_mean": float(np.mean(kernel_ms)),
+            "exact_step_replays": replays,
             "hbm_bytes_per_launch_algorithmic":
                 n * (8 * (6 * BODIES[a.model] + CONS[a.model]) + 8 + 32 + 8)}
 

@@ -104,6 +104,11 @@ hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 #define HB_KERNEL_GENERIC 1
 hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 
+/* Counters of the last fetched batch: variants that blew up, and steps the
+ * optimised kernels recomputed on the exact (library sqrt / div) path
+ * because a fast-path guard fired (0 in normal operation). */
+hb_status hb_last_launch_stats(hb_ctx* ctx, uint64_t* failed, uint64_t* exact_replays);
+
 /* ---- the drop-in call ------------------------------------------------------
  * batch_executor::run (executor.hpp:70) for `n` seeds through `steps` fixed
  * dt = kSimDt steps.  out[i] is the VariantResult of seeds[i] (seed order);

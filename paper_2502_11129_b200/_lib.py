@@ -27,6 +27,7 @@ EXPORTED = (
     "hb_build_states", "hb_run_states", "hb_stage", "hb_launch", "hb_synchronize", "hb_fetch",
     "hb_kernel_name", "hb_format_blowup", "hb_plan_allocation", "hb_plan_allocation_n",
     "hb_run_batch_multi", "hb_fp64_peak", "hb_ctx_set_kernel", "hb_check_fast_math",
+    "hb_last_launch_stats",
 )
 
 HB_KERNEL_AUTO, HB_KERNEL_GENERIC = 0, 1
@@ -72,6 +73,7 @@ def _load():
         "hb_run_batch_multi": (i32, [vp, i32, vp, i32, vp, sz, u64, vp, vp, vp, P(dbl)]),
         "hb_fp64_peak": (i32, [vp, P(dbl), P(dbl)]),
         "hb_ctx_set_kernel": (i32, [vp, i32]),
+        "hb_last_launch_stats": (i32, [vp, P(u64), P(u64)]),
         "hb_check_fast_math": (i32, [vp, vp, vp, sz, P(u64), P(u64), P(u64), P(u64)]),
     }
     for name, (res, args) in sig.items():

@@ -15,7 +15,8 @@ namespace hb {
 //         Box means "generate the initial state from seeds on the device".
 //  seeds: device seeds (n).
 //  fc:    n x {fitness, checksum bits} (16 B per variant).
-//  fail:  n x first failing step (0 = completed); fail_count += #failed.
+//  fail:  n x first failing step (0 = completed).
+//  counters: [0] += #failed variants, [1] += #exact step replays.
 //  final_state (nullable): SoA rows, ld.
 struct SimArgs {
     const double* init;
@@ -26,7 +27,7 @@ struct SimArgs {
     double dt;
     double2* fc;
     uint64_t* fail;
-    unsigned* fail_count;
+    unsigned* counters;
     double* final_state;
 };
 

@@ -245,6 +245,8 @@ struct hb_ctx {
     size_t staged_n = 0;
     bool staged_from_seeds = false;
     uint64_t last_steps = 0;
+    uint64_t last_failed = 0;
+    uint64_t last_replays = 0;
 
     hb_status fail(hb_status st, const std::string& msg) {
         err = msg;
@@ -362,7 +364,7 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
 
 hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool from_seeds,
                  double* d_final) {
-    HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, sizeof(unsigned), c->stream), "memset(count)"));
+    HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
     hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
                   c->d_fc, c->d_fail, c->d_count, d_final};
     c->last_steps = steps;
@@ -375,10 +377,12 @@ hb_status fetch(hb_ctx* c, size_t n, const uint64_t* seeds, uint64_t steps, hb_v
                 uint64_t* fail_step, bool* any_fail) {
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_fc, c->d_fc, n * sizeof(double2), cudaMemcpyDeviceToHost,
                                    c->stream), "D2H results"));
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, sizeof(unsigned), cudaMemcpyDeviceToHost,
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                    c->stream), "D2H count"));
     HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
-    const bool any = *c->h_count != 0;
+    const bool any = c->h_count[0] != 0;
+    c->last_failed = c->h_count[0];
+    c->last_replays = c->h_count[1];
     if (any) {
         HB_TRY(c->cuda(cudaMemcpy(c->h_fail, c->d_fail, n * sizeof(uint64_t), cudaMemcpyDeviceToHost),
                        "D2H fail"));
@@ -485,6 +489,13 @@ hb_status hb_ctx_set_host_threads(hb_ctx* c, int threads) {
     delete c->pool;
     c->pool = nullptr;
     c->host_threads = threads;
+    return HB_OK;
+}
+
+hb_status hb_last_launch_stats(hb_ctx* c, uint64_t* failed, uint64_t* exact_replays) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (failed) *failed = c->last_failed;
+    if (exact_replays) *exact_replays = c->last_replays;
     return HB_OK;
 }
 

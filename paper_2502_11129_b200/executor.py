@@ -185,6 +185,12 @@ class DeviceContext:
         self.check(lib.hb_fetch(self.handle, _lib.ptr(out), _lib.ptr(fail)), "hb_fetch")
         return out, fail
 
+    def last_launch_stats(self):
+        """(failed variants, exact step replays) of the last fetched batch."""
+        f, r = C.c_uint64(0), C.c_uint64(0)
+        self.check(lib.hb_last_launch_stats(self.handle, C.byref(f), C.byref(r)), "stats")
+        return int(f.value), int(r.value)
+
     def set_kernel(self, variant: int) -> None:
         """_lib.HB_KERNEL_AUTO (optimised) or _lib.HB_KERNEL_GENERIC (reference-order cross-check)."""
         self.check(lib.hb_ctx_set_kernel(self.handle, int(variant)), "hb_ctx_set_kernel")

@@ -236,7 +236,7 @@ def test_fast_math_replicas(gpu):
     sm, dm, sf, df = gpu.ctx.check_fast_math(np.abs(x), y)
     assert sm == 0 and dm == 0
     # realistic operands are essentially never flagged
-    sm2, dm2, sf2, df2 = gpu.ctx.check_fast_math(x[: n // 4], y[: n // 4])
+    sm2, dm2, sf2, df2 = gpu.ctx.check_fast_math(x[16: n // 4], y[16: n // 4])
     assert (sm2, dm2) == (0, 0) and sf2 == 0 and df2 <= 1
     # signed x (division numerators can be negative)
     sm3, dm3, _, _ = gpu.ctx.check_fast_math(x[n // 2: 3 * n // 4], y[n // 2: 3 * n // 4])
