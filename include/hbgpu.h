@@ -106,7 +106,9 @@ hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 
 /* Counters of the last fetched batch: variants that blew up, and steps the
  * optimised kernels recomputed on the exact (library sqrt / div) path
- * because a fast-path guard fired (0 in normal operation). */
+ * because a fast-path guard fired (0 in normal operation).  After several
+ * hb_launch calls without an intervening fetch they are sums over those
+ * launches (the per-variant results are always the last launch's). */
 hb_status hb_last_launch_stats(hb_ctx* ctx, uint64_t* failed, uint64_t* exact_replays);
 
 /* ---- the drop-in call ------------------------------------------------------
@@ -181,6 +183,48 @@ hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* sha
  * Times a dependent-chain-free DADD/DMUL stream on the context's device and
  * returns the sustained non-FMA FP64 op rate (ops/s) and the kernel time. */
 hb_status hb_fp64_peak(hb_ctx* ctx, double* ops_per_s, double* ms);
+
+/* ---- (mu + lambda) generation loop (ea.cpp:33-105) ------------------------
+ * run_ea with every generation's evaluation, selection (stable descending
+ * sort of fitness) and variation on the devices; only the per-generation
+ * fitness of each device's offspring slice crosses to device 0 (peer copy
+ * over NVLink) and, for models initialised on the host, the offspring seeds
+ * go through the host initialiser.  Offspring are sharded over the
+ * `count` contexts by hb_plan_allocation_n(device_times) (NULL = equal).
+ * Outputs (host): final population genomes / fitness (pop each, parents ++
+ * offspring), best fitness, phase profile; history_* (nullable) receive the
+ * population after every generation ((generations + 1) x pop).  Genomes and
+ * fitness are bit-identical to the reference run_ea over cpu_executor.
+ * A blow-up aborts with HB_BLOWUP_PARTIAL and a batch_failure-style message,
+ * as evaluate() throwing aborts run_ea. */
+typedef struct {
+    double selection_s;
+    double variation_s;
+    double evaluation_s;
+    double bookkeeping_s;
+    double total_s;
+} hb_phase_profile;
+
+hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, int kind, size_t pop,
+                    uint64_t generations, uint64_t steps, uint64_t seed, uint64_t* genomes_out,
+                    double* fitness_out, double* best_out, hb_phase_profile* profile,
+                    uint64_t* history_genomes, double* history_fitness);
+
+/* Device-pointer building blocks of the loop, for callers that keep the
+ * population in their own device memory (e.g. torch tensors; one rank per
+ * GPU with an NCCL fitness all-gather between them).  All run on the
+ * context's stream.
+ *   hb_eval_device: simulate d_seeds[0, n) (device) -> d_fitness (device);
+ *     synchronises; *n_failed = blown-up variants (HB_BLOWUP_PARTIAL if > 0).
+ *   hb_ea_init_genomes: d_genomes[i] = rng::at(seed ^ kInitKey, i).
+ *   hb_ea_select_vary: stable descending selection of the top pop/2 and
+ *     their offspring for generation g: d_next = parents ++ offspring,
+ *     d_next_fitness[0, pop/2) = parent fitness. */
+hb_status hb_eval_device(hb_ctx* ctx, int kind, const uint64_t* d_seeds, size_t n, uint64_t steps,
+                         double* d_fitness, uint64_t* n_failed);
+hb_status hb_ea_init_genomes(hb_ctx* ctx, uint64_t seed, size_t pop, uint64_t* d_genomes);
+hb_status hb_ea_select_vary(hb_ctx* ctx, const uint64_t* d_genomes, const double* d_fitness,
+                            size_t pop, uint64_t g, uint64_t* d_next, double* d_next_fitness);
 
 /* ---- fast-path self test ----------------------------------------------------
  * Evaluates the kernels' branch-free sqrt(x[i]) and x[i] / y[i] replicas and

@@ -27,10 +27,17 @@ EXPORTED = (
     "hb_build_states", "hb_run_states", "hb_stage", "hb_launch", "hb_synchronize", "hb_fetch",
     "hb_kernel_name", "hb_format_blowup", "hb_plan_allocation", "hb_plan_allocation_n",
     "hb_run_batch_multi", "hb_fp64_peak", "hb_ctx_set_kernel", "hb_check_fast_math",
-    "hb_last_launch_stats",
+    "hb_last_launch_stats", "hb_run_ea", "hb_eval_device", "hb_ea_init_genomes",
+    "hb_ea_select_vary",
 )
 
 HB_KERNEL_AUTO, HB_KERNEL_GENERIC = 0, 1
+
+
+class PhaseProfile(C.Structure):
+    _fields_ = [("selection_s", C.c_double), ("variation_s", C.c_double),
+                ("evaluation_s", C.c_double), ("bookkeeping_s", C.c_double),
+                ("total_s", C.c_double)]
 
 
 class Plan(C.Structure):
@@ -74,6 +81,11 @@ def _load():
         "hb_fp64_peak": (i32, [vp, P(dbl), P(dbl)]),
         "hb_ctx_set_kernel": (i32, [vp, i32]),
         "hb_last_launch_stats": (i32, [vp, P(u64), P(u64)]),
+        "hb_run_ea": (i32, [vp, i32, vp, i32, sz, u64, u64, u64, vp, vp, P(dbl), P(PhaseProfile),
+                            vp, vp]),
+        "hb_eval_device": (i32, [vp, i32, vp, sz, u64, vp, P(u64)]),
+        "hb_ea_init_genomes": (i32, [vp, u64, sz, vp]),
+        "hb_ea_select_vary": (i32, [vp, vp, vp, sz, u64, vp, vp]),
         "hb_check_fast_math": (i32, [vp, vp, vp, sz, P(u64), P(u64), P(u64), P(u64)]),
     }
     for name, (res, args) in sig.items():

@@ -37,4 +37,12 @@ cudaError_t launch_fp64_probe(double* scratch, int sms, int iters, cudaStream_t 
 cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, double* o0, double* o1,
                                   double* o2, double* o3, unsigned char* flags, cudaStream_t st);
 
+// Generation loop helpers (hb_ea.cu).
+cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st);
+cudaError_t ea_fitness_from_fc(const double2* fc, size_t n, double* fitness, cudaStream_t st);
+size_t ea_select_scratch_bytes(size_t pop);
+cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
+                           uint64_t* d_next, double* d_next_fit, void* scratch, size_t scratch_bytes,
+                           cudaStream_t st);
+
 }  // namespace hb

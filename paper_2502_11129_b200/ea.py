@@ -10,12 +10,16 @@ run_ea over its cpu_executor.
 """
 from __future__ import annotations
 
+import ctypes as C
 import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
-from .executor import BatchExecutor, BatchRequest, ModelKind
+from . import _lib
+from ._lib import lib
+from .executor import (BatchExecutor, BatchFailure, BatchRequest, GpuExecutor, ModelKind,
+                       MultiGpuExecutor)
 
 K_INIT_KEY = 0x8F5D4C3B2A190807
 K_CHILD_KEY = 0x243F6A8885A308D3
@@ -80,8 +84,14 @@ def _evaluate(kind, genomes, steps, executor: BatchExecutor) -> np.ndarray:
 
 
 def run_ea(kind: ModelKind, population_size: int, generations: int, steps: int,
-           executor: BatchExecutor, seed: int = 0, keep_history: bool = False) -> EaResult:
-    """ea.cpp:33-105."""
+           executor: BatchExecutor, seed: int = 0, keep_history: bool = False,
+           native: bool = True) -> EaResult:
+    """ea.cpp:33-105.  With a GPU executor (and native=True) the whole loop runs
+    natively (hb_run_ea: device-side selection / variation, offspring sharded
+    over the executor's devices); any other BatchExecutor goes through the
+    same loop in Python."""
+    if native and isinstance(executor, (GpuExecutor, MultiGpuExecutor)):
+        return run_ea_native(kind, population_size, generations, steps, executor, seed, keep_history)
     if population_size < 2 or population_size % 2 != 0:
         raise ValueError("run_ea: population_size must be even and >= 2")
     if generations < 1:
@@ -132,6 +142,46 @@ def run_ea(kind: ModelKind, population_size: int, generations: int, steps: int,
     if prof.total_s > accounted:
         prof.bookkeeping_s += prof.total_s - accounted
     return EaResult(pop, prof, float(np.max(pop.fitnesses)), history)
+
+
+def run_ea_native(kind: ModelKind, population_size: int, generations: int, steps: int,
+                  executor, seed: int = 0, keep_history: bool = False,
+                  device_times=None) -> EaResult:
+    """hb_run_ea over the executor's device contexts."""
+    if population_size < 2 or population_size % 2 != 0:
+        raise ValueError("run_ea: population_size must be even and >= 2")
+    if generations < 1:
+        raise ValueError("run_ea: generations must be >= 1")
+    ctxs = [executor.ctx] if isinstance(executor, GpuExecutor) else list(executor.ctxs)
+    cnt = len(ctxs)
+    handles = (C.c_void_p * cnt)(*[c.handle for c in ctxs])
+    times = None
+    if device_times is not None:
+        times = np.ascontiguousarray(device_times, dtype=np.float64)
+    elif isinstance(executor, MultiGpuExecutor) and executor.shares is not None:
+        times = None
+    gen = np.empty(population_size, dtype=np.uint64)
+    fit = np.empty(population_size)
+    best = C.c_double(0)
+    prof = _lib.PhaseProfile()
+    hg = hf = None
+    if keep_history:
+        hg = np.empty((generations + 1, population_size), dtype=np.uint64)
+        hf = np.empty((generations + 1, population_size))
+    st = lib.hb_run_ea(C.cast(handles, C.c_void_p), cnt, None if times is None else _lib.ptr(times),
+                       int(kind), population_size, int(generations), int(steps), int(seed),
+                       _lib.ptr(gen), _lib.ptr(fit), C.byref(best), C.byref(prof),
+                       None if hg is None else _lib.ptr(hg), None if hf is None else _lib.ptr(hf))
+    if st == _lib.HB_INVALID_ARG:
+        raise ValueError(ctxs[0].error())
+    if st == _lib.HB_BLOWUP_PARTIAL:
+        raise RuntimeError(ctxs[0].error())
+    if st != _lib.HB_OK:
+        raise RuntimeError(f"hb_run_ea failed [{st}]: {ctxs[0].error()}")
+    profile = PhaseProfile(prof.selection_s, prof.variation_s, prof.evaluation_s,
+                           prof.bookkeeping_s, prof.total_s)
+    history = [] if hg is None else [(hg[g], hf[g]) for g in range(generations + 1)]
+    return EaResult(Population(gen, fit, generations), profile, float(best.value), history)
 
 
 def report_profile(profile: PhaseProfile) -> str:
