@@ -104,6 +104,16 @@ hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 #define HB_KERNEL_GENERIC 1
 hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 
+/* Page-locked host memory (cudaHostAlloc, portable).  hb_run_batch / hb_fetch
+ * DMA the results straight into an `out` buffer allocated here (no staging
+ * copy); any other buffer goes through the context's staging buffer. */
+void* hb_host_alloc(size_t bytes);
+void hb_host_free(void* ptr);
+
+/* Failure steps of the last fetched batch (n entries; 0 = completed), for
+ * callers that passed fail_step = NULL and got HB_BLOWUP_PARTIAL. */
+hb_status hb_last_fail_steps(hb_ctx* ctx, uint64_t* fail_step, size_t n);
+
 /* Counters of the last fetched batch: variants that blew up, and steps the
  * optimised kernels recomputed on the exact (library sqrt / div) path
  * because a fast-path guard fired (0 in normal operation).  After several

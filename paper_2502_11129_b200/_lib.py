@@ -8,6 +8,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
+import weakref
 
 import numpy as np
 
@@ -28,7 +30,7 @@ EXPORTED = (
     "hb_kernel_name", "hb_format_blowup", "hb_plan_allocation", "hb_plan_allocation_n",
     "hb_run_batch_multi", "hb_fp64_peak", "hb_ctx_set_kernel", "hb_check_fast_math",
     "hb_last_launch_stats", "hb_run_ea", "hb_eval_device", "hb_ea_init_genomes",
-    "hb_ea_select_vary",
+    "hb_ea_select_vary", "hb_host_alloc", "hb_host_free", "hb_last_fail_steps",
 )
 
 HB_KERNEL_AUTO, HB_KERNEL_GENERIC = 0, 1
@@ -86,6 +88,9 @@ def _load():
         "hb_eval_device": (i32, [vp, i32, vp, sz, u64, vp, P(u64)]),
         "hb_ea_init_genomes": (i32, [vp, u64, sz, vp]),
         "hb_ea_select_vary": (i32, [vp, vp, vp, sz, u64, vp, vp]),
+        "hb_host_alloc": (vp, [sz]),
+        "hb_host_free": (None, [vp]),
+        "hb_last_fail_steps": (i32, [vp, vp, sz]),
         "hb_check_fast_math": (i32, [vp, vp, vp, sz, P(u64), P(u64), P(u64), P(u64)]),
     }
     for name, (res, args) in sig.items():
@@ -96,6 +101,39 @@ def _load():
 
 
 lib = _load()
+
+
+class PinnedPool:
+    """Reusable page-locked result buffers.  Arrays handed out view pinned
+    memory; when an array (and every view of it) is garbage-collected its
+    buffer returns to the pool, so steady-state batches neither page-fault
+    nor need a staging copy (the device DMAs straight into the array)."""
+
+    def __init__(self):
+        self._free = {}
+        self._lock = threading.Lock()
+
+    def empty(self, n: int, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        nbytes = max(int(n) * dtype.itemsize, 1)
+        cls = 1 << max(12, (nbytes - 1).bit_length())
+        with self._lock:
+            lst = self._free.get(cls)
+            p = lst.pop() if lst else None
+        if p is None:
+            p = lib.hb_host_alloc(cls)
+            if not p:
+                return np.empty(n, dtype=dtype)  # not pinned: results go through staging
+        raw = (C.c_char * cls).from_address(p)
+        weakref.finalize(raw, self._release, cls, p)
+        return np.frombuffer(raw, dtype=dtype, count=int(n))
+
+    def _release(self, cls, p):
+        with self._lock:
+            self._free.setdefault(cls, []).append(p)
+
+
+pinned = PinnedPool()
 
 
 def ptr(a: np.ndarray) -> int:

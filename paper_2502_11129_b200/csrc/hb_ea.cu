@@ -46,9 +46,9 @@ __global__ void select_vary_kernel(const uint64_t* genomes, const double* sorted
     next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
 }
 
-__global__ void fitness_from_fc_kernel(const double2* fc, size_t n, double* fitness) {
+__global__ void fitness_from_results_kernel(const hb_variant_result* out, size_t n, double* fitness) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i < n) fitness[i] = fc[i].x;
+    if (i < n) fitness[i] = out[i].fitness;
 }
 
 unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
@@ -61,9 +61,10 @@ cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cuda
     return cudaGetLastError();
 }
 
-cudaError_t ea_fitness_from_fc(const double2* fc, size_t n, double* fitness, cudaStream_t st) {
+cudaError_t ea_fitness_from_results(const hb_variant_result* out, size_t n, double* fitness,
+                                    cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    fitness_from_fc_kernel<<<blocks_for(n), 256, 0, st>>>(fc, n, fitness);
+    fitness_from_results_kernel<<<blocks_for(n), 256, 0, st>>>(out, n, fitness);
     return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ namespace hb {
 //  init:  SoA rows (state_rows(kind) x ld doubles), read-only; nullptr for
 //         Box means "generate the initial state from seeds on the device".
 //  seeds: device seeds (n).
-//  fc:    n x {fitness, checksum bits} (16 B per variant).
+//  out:   n x VariantResult (32 B, the reference layout).
 //  fail:  n x first failing step (0 = completed).
 //  counters: [0] += #failed variants, [1] += #exact step replays.
 //  final_state (nullable): SoA rows, ld.
@@ -25,7 +25,7 @@ struct SimArgs {
     size_t ld;
     uint64_t steps;
     double dt;
-    double2* fc;
+    hb_variant_result* out;
     uint64_t* fail;
     unsigned* counters;
     double* final_state;
@@ -39,7 +39,8 @@ cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, do
 
 // Generation loop helpers (hb_ea.cu).
 cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st);
-cudaError_t ea_fitness_from_fc(const double2* fc, size_t n, double* fitness, cudaStream_t st);
+cudaError_t ea_fitness_from_results(const hb_variant_result* out, size_t n, double* fitness,
+                                    cudaStream_t st);
 size_t ea_select_scratch_bytes(size_t pop);
 cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
                            uint64_t* d_next, double* d_next_fit, void* scratch, size_t scratch_bytes,

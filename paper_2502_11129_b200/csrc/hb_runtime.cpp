@@ -18,6 +18,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -223,7 +224,7 @@ struct hb_ctx {
     double* d_init = nullptr;
     size_t d_init_cap = 0;  // doubles
     uint64_t* d_seeds = nullptr;
-    double2* d_fc = nullptr;   // {fitness, checksum bits} per variant
+    hb_variant_result* d_out = nullptr;  // 32-byte results per variant
     uint64_t* d_fail = nullptr;
     size_t d_n_cap = 0;
     unsigned* d_count = nullptr;  // failed-variant counter
@@ -237,7 +238,7 @@ struct hb_ctx {
     double* h_init = nullptr;
     size_t h_init_cap = 0;
     uint64_t* h_seeds = nullptr;
-    double2* h_fc = nullptr;
+    hb_variant_result* h_out = nullptr;
     uint64_t* h_fail = nullptr;
     size_t h_n_cap = 0;
     unsigned* h_count = nullptr;
@@ -249,6 +250,7 @@ struct hb_ctx {
     uint64_t last_steps = 0;
     uint64_t last_failed = 0;
     uint64_t last_replays = 0;
+    size_t last_n = 0;
     bool counters_dirty = true;  // device counters need a reset before the next launch
 
     hb_status fail(hb_status st, const std::string& msg) {
@@ -296,20 +298,20 @@ hb_status ensure_capacity(hb_ctx* c, int kind, size_t n, bool need_init) {
         }
     }
     if (n > c->d_n_cap) {
-        cudaFree(c->d_seeds); cudaFree(c->d_fc); cudaFree(c->d_fail);
-        c->d_seeds = nullptr; c->d_fc = nullptr; c->d_fail = nullptr;
+        cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
+        c->d_seeds = nullptr; c->d_out = nullptr; c->d_fail = nullptr;
         const size_t cap = std::max(n, c->d_n_cap * 2);
         HB_TRY(c->cuda(cudaMalloc(&c->d_seeds, cap * sizeof(uint64_t)), "cudaMalloc(seeds)"));
-        HB_TRY(c->cuda(cudaMalloc(&c->d_fc, cap * sizeof(double2)), "cudaMalloc(fc)"));
+        HB_TRY(c->cuda(cudaMalloc(&c->d_out, cap * sizeof(hb_variant_result)), "cudaMalloc(out)"));
         HB_TRY(c->cuda(cudaMalloc(&c->d_fail, cap * sizeof(uint64_t)), "cudaMalloc(fail)"));
         c->d_n_cap = cap;
     }
     if (n > c->h_n_cap) {
-        cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_fc); cudaFreeHost(c->h_fail);
-        c->h_seeds = nullptr; c->h_fc = nullptr; c->h_fail = nullptr;
+        cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
+        c->h_seeds = nullptr; c->h_out = nullptr; c->h_fail = nullptr;
         const size_t cap = std::max(n, c->h_n_cap * 2);
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_seeds, cap * sizeof(uint64_t), 0), "cudaHostAlloc(seeds)"));
-        HB_TRY(c->cuda(cudaHostAlloc(&c->h_fc, cap * sizeof(double2), 0), "cudaHostAlloc(fc)"));
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_out, cap * sizeof(hb_variant_result), 0), "cudaHostAlloc(out)"));
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_fail, cap * sizeof(uint64_t), 0), "cudaHostAlloc(fail)"));
         c->h_n_cap = cap;
     }
@@ -338,10 +340,38 @@ bool init_on_device(const hb_ctx* c, int kind) {
 
 constexpr size_t kParallelCopyMin = 2048;  // min items per host thread for copies / assembly
 
+bool trace_on() {
+    static int on = -1;
+    if (on < 0) on = getenv("HB_TRACE") != nullptr;
+    return on == 1;
+}
+
+struct Trace {
+    const char* what;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    std::chrono::steady_clock::time_point last = t0;
+    std::string line;
+    explicit Trace(const char* w) : what(w) {}
+    void mark(const char* tag) {
+        if (!trace_on()) return;
+        const auto now = std::chrono::steady_clock::now();
+        char buf[64];
+        std::snprintf(buf, sizeof buf, " %s=%.1fus", tag,
+                      std::chrono::duration<double, std::micro>(now - last).count());
+        line += buf;
+        last = now;
+    }
+    ~Trace() {
+        if (trace_on()) std::fprintf(stderr, "[hb] %s%s\n", what, line.c_str());
+    }
+};
+
 // Seeds (+ host-built initial states) into pinned memory, async H2D.
 hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
+    Trace tr("stage");
     const bool dev_init = init_on_device(c, kind);
     HB_TRY(ensure_capacity(c, kind, n, !dev_init));
+    tr.mark("alloc");
     uint64_t* hs = c->h_seeds;
     if (dev_init) {
         pool_of(c).run(n, [&](size_t b, size_t e) {
@@ -357,8 +387,10 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
         HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
                                        cudaMemcpyHostToDevice, c->stream), "H2D init"));
     }
+    tr.mark("host");
     HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, c->h_seeds, n * sizeof(uint64_t),
                                    cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+    tr.mark("h2d_enqueue");
     c->staged_kind = kind;
     c->staged_n = n;
     c->staged_from_seeds = dev_init;
@@ -372,51 +404,60 @@ hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool 
         c->counters_dirty = false;
     }
     hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
-                  c->d_fc, c->d_fail, c->d_count, d_final};
+                  c->d_out, c->d_fail, c->d_count, d_final};
     c->last_steps = steps;
     return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch");
 }
 
 // D2H of the compact records + failure count; assemble 32-byte
 // VariantResults (seed and steps are known on the host) in seed order.
-hb_status fetch(hb_ctx* c, size_t n, const uint64_t* seeds, uint64_t steps, hb_variant_result* out,
-                uint64_t* fail_step, bool* any_fail) {
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_fc, c->d_fc, n * sizeof(double2), cudaMemcpyDeviceToHost,
-                                   c->stream), "D2H results"));
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+// D2H of the 32-byte results (directly into `out` when it is pinned, else
+// through the pinned staging buffer) + failure counters; the per-variant
+// failure steps only when something blew up.
+hb_status fetch(hb_ctx* c, size_t n, hb_variant_result* out, uint64_t* fail_step, bool* any_fail) {
+    Trace tr("fetch");
+    const bool direct = is_pinned(out);
+    HB_TRY(c->cuda(cudaMemcpyAsync(direct ? out : c->h_out, c->d_out, n * sizeof(hb_variant_result),
+                                   cudaMemcpyDeviceToHost, c->stream), "D2H results"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                    c->stream), "D2H count"));
+    tr.mark(direct ? "enqueue(direct)" : "enqueue(staged)");
     HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+    tr.mark("sync");
     const bool any = c->h_count[0] != 0;
     c->last_failed = c->h_count[0];
     c->last_replays = c->h_count[1];
+    c->last_n = n;
     // Reset the counters now (stream-ordered), so the next launch needs no
     // extra operation on its critical path.
     c->counters_dirty = (c->h_count[0] | c->h_count[1]) != 0;
-    if (any) {
-        HB_TRY(c->cuda(cudaMemcpy(c->h_fail, c->d_fail, n * sizeof(uint64_t), cudaMemcpyDeviceToHost),
-                       "D2H fail"));
+    if (any || fail_step) {
+        if (any) {
+            HB_TRY(c->cuda(cudaMemcpy(c->h_fail, c->d_fail, n * sizeof(uint64_t), cudaMemcpyDeviceToHost),
+                           "D2H fail"));
+        }
     }
-    const double2* fc = c->h_fc;
+    const hb_variant_result* src = c->h_out;
     const uint64_t* hf = c->h_fail;
-    pool_of(c).run(n, [&](size_t b, size_t e) {
-        for (size_t i = b; i < e; ++i) {
-            hb_variant_result r;
-            r.seed = seeds[i];
-            r.fitness = fc[i].x;
-            r.checksum = static_cast<uint64_t>(__double_as_longlong_host(fc[i].y));
-            r.steps_executed = steps;
-            if (any && hf[i]) {
-                r.fitness = 0.0;
-                r.checksum = 0;
-                r.steps_executed = hf[i];
+    if (!direct || fail_step) {
+        pool_of(c).run(n, [&](size_t b, size_t e) {
+            if (!direct) std::memcpy(out + b, src + b, (e - b) * sizeof(hb_variant_result));
+            if (fail_step) {
+                if (any) std::memcpy(fail_step + b, hf + b, (e - b) * sizeof(uint64_t));
+                else std::memset(fail_step + b, 0, (e - b) * sizeof(uint64_t));
             }
-            out[i] = r;
-        }
-        if (fail_step) {
-            if (any) std::memcpy(fail_step + b, hf + b, (e - b) * sizeof(uint64_t));
-            else std::memset(fail_step + b, 0, (e - b) * sizeof(uint64_t));
-        }
-    }, kParallelCopyMin);
+        }, kParallelCopyMin);
+    }
+    tr.mark("host");
     *any_fail = any;
     return HB_OK;
 }
@@ -480,9 +521,9 @@ void hb_ctx_destroy(hb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_fc); cudaFree(c->d_fail);
+    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
     cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count); cudaFree(c->d_ea_fit);
-    cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_fc); cudaFreeHost(c->h_fail);
+    cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
     cudaFreeHost(c->h_count);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c->pool;
@@ -498,6 +539,28 @@ hb_status hb_ctx_set_host_threads(hb_ctx* c, int threads) {
     delete c->pool;
     c->pool = nullptr;
     c->host_threads = threads;
+    return HB_OK;
+}
+
+void* hb_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0 || cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        set_global(HB_CUDA_ERROR, "cudaHostAlloc failed");
+        return nullptr;
+    }
+    return p;
+}
+
+void hb_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+hb_status hb_last_fail_steps(hb_ctx* c, uint64_t* fail_step, size_t n) {
+    if (!c || !fail_step) return set_global(HB_INVALID_ARG, "bad arguments");
+    if (n > c->last_n) return c->fail(HB_INVALID_ARG, "more failure steps requested than the batch had");
+    if (c->last_failed) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
+    else std::memset(fail_step, 0, n * sizeof(uint64_t));
     return HB_OK;
 }
 
@@ -530,7 +593,7 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
     HB_TRY(stage_inputs(c, kind, seeds, n));
     HB_TRY(launch(c, kind, n, steps, hb::kSimDt, c->staged_from_seeds, nullptr));
     bool any = false;
-    HB_TRY(fetch(c, n, seeds, steps, out, fail_step, &any));
+    HB_TRY(fetch(c, n, out, fail_step, &any));
     if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
     return HB_OK;
@@ -560,7 +623,7 @@ hb_status hb_run_states(hb_ctx* c, int kind, const double* init_soa, size_t n, u
     c->staged_kind = -1;
     HB_TRY(launch(c, kind, n, steps, dt, false, final_soa ? c->d_final : nullptr));
     bool any = false;
-    HB_TRY(fetch(c, n, sd, steps, out, fail_step, &any));
+    HB_TRY(fetch(c, n, out, fail_step, &any));
     if (final_soa) {
         HB_TRY(c->cuda(cudaMemcpy(final_soa, c->d_final, bytes, cudaMemcpyDeviceToHost), "D2H final"));
     }
@@ -591,7 +654,7 @@ hb_status hb_fetch(hb_ctx* c, hb_variant_result* out, uint64_t* fail_step) {
     if (!c || !out) return set_global(HB_INVALID_ARG, "bad arguments");
     if (c->staged_kind < 0) return c->fail(HB_INVALID_ARG, "hb_fetch: no staged batch");
     bool any = false;
-    HB_TRY(fetch(c, c->staged_n, c->h_seeds, c->last_steps, out, fail_step, &any));
+    HB_TRY(fetch(c, c->staged_n, out, fail_step, &any));
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
     return HB_OK;
 }
@@ -831,9 +894,9 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
         c->counters_dirty = false;
     }
     hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
-                  c->d_fc, c->d_fail, c->d_count, nullptr};
+                  c->d_out, c->d_fail, c->d_count, nullptr};
     HB_TRY(c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
-    HB_TRY(c->cuda(hb::ea_fitness_from_fc(c->d_fc, n, d_fitness, c->stream), "fitness gather"));
+    HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                    c->stream), "D2H count"));
     return HB_OK;

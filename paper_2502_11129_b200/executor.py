@@ -227,12 +227,14 @@ class GpuExecutor(BatchExecutor):
         """(results, fail_step, wall_s, status) without raising on blow-up."""
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
         n = len(seeds)
-        out = np.empty(n, dtype=RESULT_DTYPE)
-        fail = np.empty(n, dtype=np.uint64)
+        out = _lib.pinned.empty(n, RESULT_DTYPE)
         wall = C.c_double(0)
         st = lib.hb_run_batch(self.ctx.handle, int(kind), _lib.ptr(seeds), n, int(steps),
-                              _lib.ptr(out), _lib.ptr(fail), C.byref(wall))
+                              _lib.ptr(out), None, C.byref(wall))
         self.ctx.check(st, "hb_run_batch")
+        fail = np.zeros(n, dtype=np.uint64)
+        if st == _lib.HB_BLOWUP_PARTIAL:
+            self.ctx.check(lib.hb_last_fail_steps(self.ctx.handle, _lib.ptr(fail), n), "fail steps")
         return out, fail, wall.value, st
 
     def run(self, request: BatchRequest) -> BatchResult:
