@@ -293,12 +293,18 @@ def run_ours(a, ws, rank, local):
             "kernel_ms_mean": float(np.mean(kernel_ms)),
             "exact_step_replays": replays,
             "hbm_bytes_per_launch_algorithmic":
-                n * (8 * (6 * BODIES[a.model] + CONS[a.model]) + 8 + 32 + 8)}
+                n * ((0 if a.model == "box" else 8 * (6 * BODIES[a.model] + CONS[a.model]))
+                     + 8 + 32 + 8)}
 
     # ---- e2e through the drop-in call (host seeds -> host results) ----
     e2e = None
     if not a.no_e2e:
-        req = hb.BatchRequest(kind, seeds, a.sim_steps)
+        # the step's inputs live in page-locked host memory (the caller's
+        # seeds); results come back into pinned result buffers
+        from paper_2502_11129_b200 import _lib
+        host_seeds = _lib.pinned.empty(n, np.uint64)
+        host_seeds[:] = seeds
+        req = hb.BatchRequest(kind, host_seeds, a.sim_steps)
         for _ in range(a.warmup):
             ex.run(req)
         barrier()
@@ -311,9 +317,10 @@ def run_ours(a, ws, rank, local):
         t_e2e = max_over_ranks(t_e2e)
         assert np.array_equal(r.results, out)
         rows = 6 * BODIES[a.model] + CONS[a.model]
+        init_bytes = 0 if a.model == "box" else 8 * rows  # Box initial state is built on the device
         e2e = {"value": units * a.steps / t_e2e, "unit": "variant-steps/s",
-               "h2d_bytes_per_step": n_total * (8 * rows + 8),
-               "d2h_bytes_per_step": n_total * (32 + 8),
+               "h2d_bytes_per_step": n_total * (8 + init_bytes),
+               "d2h_bytes_per_step": n_total * 32 + 8 * ws,
                "ms_per_step": 1e3 * t_e2e / a.steps,
                "path": "GpuExecutor.run -> hb_run_batch (host init + H2D + kernel + D2H)"}
 

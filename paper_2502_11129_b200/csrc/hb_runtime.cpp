@@ -340,6 +340,15 @@ bool init_on_device(const hb_ctx* c, int kind) {
 
 constexpr size_t kParallelCopyMin = 2048;  // min items per host thread for copies / assembly
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
 bool trace_on() {
     static int on = -1;
     if (on < 0) on = getenv("HB_TRACE") != nullptr;
@@ -366,29 +375,33 @@ struct Trace {
     }
 };
 
-// Seeds (+ host-built initial states) into pinned memory, async H2D.
+// Seeds (+ host-built initial states) to the device.  Seeds already in
+// page-locked memory are DMA'd directly; others are copied into the pinned
+// staging buffer first (in parallel with the host initialiser).
 hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
     Trace tr("stage");
     const bool dev_init = init_on_device(c, kind);
     HB_TRY(ensure_capacity(c, kind, n, !dev_init));
     tr.mark("alloc");
+    const bool direct = is_pinned(seeds);
     uint64_t* hs = c->h_seeds;
     if (dev_init) {
-        pool_of(c).run(n, [&](size_t b, size_t e) {
-            std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
-        }, kParallelCopyMin);
+        if (!direct)
+            pool_of(c).run(n, [&](size_t b, size_t e) {
+                std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
+            }, kParallelCopyMin);
     } else {
         double* soa = c->h_init;
         pool_of(c).run(n, [&](size_t b, size_t e) {
-            std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
+            if (!direct) std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
             build_range(kind, seeds, b, e, soa, n);
         }, 64);
         const size_t rows = static_cast<size_t>(hb::state_rows(kind));
         HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
                                        cudaMemcpyHostToDevice, c->stream), "H2D init"));
     }
-    tr.mark("host");
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, c->h_seeds, n * sizeof(uint64_t),
+    tr.mark(direct ? "host(direct)" : "host(staged)");
+    HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, direct ? seeds : c->h_seeds, n * sizeof(uint64_t),
                                    cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
     tr.mark("h2d_enqueue");
     c->staged_kind = kind;
@@ -411,15 +424,6 @@ hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool 
 
 // D2H of the compact records + failure count; assemble 32-byte
 // VariantResults (seed and steps are known on the host) in seed order.
-bool is_pinned(const void* p) {
-    cudaPointerAttributes at;
-    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return at.type == cudaMemoryTypeHost;
-}
-
 // D2H of the 32-byte results (directly into `out` when it is pinned, else
 // through the pinned staging buffer) + failure counters; the per-variant
 // failure steps only when something blew up.
