@@ -1,0 +1,72 @@
+"""World-size-2 gloo tests (CPU) of the multi-process path: per-rank
+contiguous shards from the N-way splitter, the fitness all-gather, and the
+sharded generation loop — identical to the single-process run_ea."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import paper_2502_11129_b200 as hb
+from paper_2502_11129_b200 import distributed as hbd
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, kind, pop, gens, steps, times, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers import OracleExecutor
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        r = hbd.run_ea_sharded(kind, pop, gens, steps, OracleExecutor(1), dist, seed=3, times=times)
+        b = hbd.shard_bounds(1000, world, times)
+        q.put((rank, r.population.genomes.tolist(), r.population.fitnesses.tolist(), b.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("times", [None, [1.0, 3.0]])
+def test_sharded_ea_world2_equals_single_process(times):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    kind, pop, gens, steps = 1, 64, 3, 40
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, pop, gens, steps, times, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers import OracleExecutor
+    ref = hb.run_ea(kind, pop, gens, steps, OracleExecutor(2), seed=3)
+    for rank, g, f, b in out:
+        assert g == ref.population.genomes.tolist()
+        assert np.array_equal(np.array(f), ref.population.fitnesses)
+        assert b[0] == 0 and b[-1] == 1000
+    expect = hbd.shard_bounds(1000, 2, times).tolist()
+    assert all(o[3] == expect for o in out)
+    if times is not None:
+        assert expect == [0, 750, 1000]  # throughput-proportional (1/t)
+
+
+def test_shard_bounds_cover_contiguously():
+    for world in (1, 2, 3, 8):
+        for n in (1, 7, 1000, 65536):
+            b = hbd.shard_bounds(n, world)
+            assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
+            assert np.max(np.diff(b)) - np.min(np.diff(b)) <= world
