@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--model", default="box", choices=MODELS)
     ap.add_argument("--variants", type=int, default=16384, help="variants per GPU")
     ap.add_argument("--sim-steps", type=int, default=1000)
+    ap.add_argument("--workload", default="batch", choices=["batch", "ea"],
+                    help="batch = one simulate() pass per step (configs[1]); ea = full generation "
+                         "loop per step (configs[4]: evaluate, fitness gather, select)")
+    ap.add_argument("--population", type=int, default=65536, help="ea: population size (global)")
+    ap.add_argument("--generations", type=int, default=5, help="ea: generations per step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -211,14 +216,20 @@ def run_ours(a, ws, rank, local):
     import paper_2502_11129_b200 as hb
 
     dist = None
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only for gloo tests
+    torch.cuda.set_device(local)
+    backend = os.environ.get("HB_DIST_BACKEND", "nccl")
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")
     kind = hb.parse_model_kind(a.model)
+    if a.workload == "ea":
+        return run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind)
 
     # Global batch + N-way splitter (equal calibrated GPUs -> equal shares).
     n_total = a.variants * ws
@@ -239,7 +250,7 @@ def run_ours(a, ws, rank, local):
     def max_over_ranks(x: float) -> float:
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -346,6 +357,77 @@ def run_ours(a, ws, rank, local):
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": a.steps, "e2e_gpu_launches": a.steps if e2e else 0,
                 "bracket_wall_s": wall_region, "parity": "bit-exact FP64 vs reference"}
+        print(json.dumps(line))
+    ex.ctx.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
+    """configs[4]: the full (mu + lambda) generation loop.  One bench step =
+    one run_ea of `--generations` generations over `--population` genomes
+    (pop + G * pop/2 variants simulated through `--sim-steps` steps each).
+    N = 1: the native device loop (hb_run_ea: device selection / variation).
+    N > 1: one rank per GPU, offspring sharded by the N-way splitter, fitness
+    all-gathered over NCCL every generation; max wall over ranks."""
+    import torch
+    import paper_2502_11129_b200 as hb
+    from paper_2502_11129_b200 import distributed as hbd
+    ex = hb.GpuExecutor(local)
+    pop, G = a.population, a.generations
+    evaluated = pop + G * (pop // 2)
+
+    def one():
+        if ws == 1:
+            return hb.run_ea(kind, pop, G, a.sim_steps, ex, seed=0)
+        return hbd.run_ea_sharded(kind, pop, G, a.sim_steps, ex, dist, seed=0,
+                                  device=red_dev if red_dev.type == "cuda" else None)
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(a.warmup):
+        r = one()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    profs = []
+    for _ in range(a.steps):
+        r = one()
+        profs.append(r.profile)
+    torch.cuda.synchronize(dev)
+    t = max_over_ranks(time.perf_counter() - t0)
+    clk = clocks.stop()
+    value = evaluated * a.sim_steps * a.steps / t
+    if rank == 0:
+        ev = sum(p.evaluation_s for p in profs)
+        tot = sum(p.total_s for p in profs)
+        line = {"metric": METRIC, "value": value, "unit": "variant-steps/s", "n_gpus": ws,
+                "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (genomes rng::at(seed ^ kInitKey, i), ea.cpp:48-52)",
+                "config": {"workload": f"ea: run_ea {a.model} pop {pop} x {G} generations x "
+                                       f"{a.sim_steps} steps (BASELINE configs[4])",
+                           "model": a.model, "population": pop, "generations": G,
+                           "sim_steps": a.sim_steps, "variants_simulated_per_step": evaluated,
+                           "parallelism": f"dp{ws} offspring shards (plan_allocation_n) + "
+                                          "per-generation fitness all-gather"},
+                "e2e": {"value": value, "unit": "variant-steps/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 16 * pop,
+                        "path": "run_ea -> hb_run_ea (genomes created and selected on the device; "
+                                "final population D2H)" if ws == 1 else
+                                "run_ea_sharded (host selection; NCCL fitness all-gather)"},
+                "evaluation_fraction": ev / tot if tot else None,
+                "best_fitness": r.best_fitness, "clocks": clk,
+                "gpu_launches": a.steps * (G + 1) * (1 if ws == 1 else 1),
+                "parity": "genomes + fitness bit-identical to reference run_ea"}
         print(json.dumps(line))
     ex.ctx.close()
     if dist is not None:
