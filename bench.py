@@ -181,6 +181,34 @@ def run_reference(a, ws, rank):
                           "unavailable": "oracle/_ref/libhetbench_ref.so was not built"}))
         return
     cores = O.ref_hardware_concurrency()
+    if a.workload == "ea":
+        # the reference's own run_ea over cpu_executor(workers = all threads)
+        per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[k]
+        G = a.generations
+        pop = a.population
+        budget = 10.0 * cores / (per_vs_core_ns * 1e-9) / a.sim_steps  # variants per step
+        while pop > 64 * cores and (pop + G * pop // 2) > budget:
+            pop //= 2
+        evaluated = pop + G * (pop // 2)
+        for _ in range(a.warmup):
+            O.ref_run_ea(k, pop, G, a.sim_steps, 0, workers=0)
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            O.ref_run_ea(k, pop, G, a.sim_steps, 0, workers=0)
+        total = time.perf_counter() - t0
+        value = evaluated * a.sim_steps * a.steps / total
+        sample = (f"reference run_ea {a.model} pop {pop} (of {a.population}) x {G} generations x "
+                  f"{a.sim_steps} steps over cpu_executor(workers=0 -> {cores} threads)")
+        base["config"].update({"workload": f"ea: run_ea {a.model} pop {a.population} x {G} "
+                                           f"generations x {a.sim_steps} steps (BASELINE configs[4])"})
+        base.update({"value": value, "ms_per_step": 1e3 * total / a.steps,
+                     "cpu_baseline": {"value": value, "unit": "variant-steps/s", "cores": cores,
+                                      "kind": "reference", "sample": sample},
+                     "e2e": {"value": value, "unit": "variant-steps/s", "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0},
+                     "vs_baseline": None, "scaling": "strong"})
+        print(json.dumps(base))
+        return
     n_total = a.variants * a.gpus
     # bounded per-step sample: ~10 s of host time per step at most
     per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[k]

@@ -128,9 +128,9 @@ def test_blowup_surfaces_as_batch_failure(gpu, golden):
     assert msg == golden["blowup_messages"][0]["message"] + " (seed 3)"
 
 
-def test_blowup_batch_failure_through_run():
-    """A real batch_failure raised by GpuExecutor.run (drive a kind whose
-    state we cannot blow up from a seed by running from the blown state)."""
+def test_batch_failure_message_format():
+    """batch_failure's what(): failed sorted by seed, "(+k more)", first
+    message (executor.cpp:20-28)."""
     err = hb.BatchFailure([(7, "b"), (3, "a")], np.zeros(0, dtype=hb.RESULT_DTYPE))
     assert str(err) == "batch failed for seed 3 (+1 more): a"
     assert err.failed == [(3, "a"), (7, "b")]
