@@ -37,12 +37,15 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 METRIC = "variant-steps/sec (whole box) vs #variants & steps; speedup over host-CPU ref"
-MODELS = ("box", "box_and_ball", "arm_with_rope", "humanoid")
+MODELS = ("box", "box_and_ball", "arm_with_rope", "humanoid", "cpg_hinge")
 # Algorithmic FP64 ops per variant-step (add/sub/mul/div/sqrt = 1,
 # compares excluded): 16n + 8m*(19 + sqrt + div).
-W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240}
-BODIES = {"box": 1, "box_and_ball": 2, "arm_with_rope": 12, "humanoid": 32}
-CONS = {"box": 0, "box_and_ball": 1, "arm_with_rope": 11, "humanoid": 46}
+# cpg_hinge (not in the reference): 16*9 + 8*12*21 + 4 joints x 11 CPG/actuation ops.
+W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240, "cpg_hinge": 2204}
+BODIES = {"box": 1, "box_and_ball": 2, "arm_with_rope": 12, "humanoid": 32, "cpg_hinge": 9}
+CONS = {"box": 0, "box_and_ball": 1, "arm_with_rope": 11, "humanoid": 46, "cpg_hinge": 12}
+EXTRA_ROWS = {"cpg_hinge": 16}
+PER_VS_CORE_NS = {0: 58, 1: 298, 2: 2110, 3: 8190, 4: 1700}
 
 
 def parse():
@@ -143,10 +146,12 @@ def cpu_reference_rate(model_idx, n, sim_steps, reps=3):
     """Reference cpu_executor(workers = hardware_concurrency) on the host; best
     of `reps` runs of a bounded sample (the full workload when it is small)."""
     import oracle as O
+    if model_idx == 4:
+        return cpu_port_rate(model_idx, n, sim_steps, reps)
     if not O.ref_available():
         return None
     cores = O.ref_hardware_concurrency()
-    per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[model_idx]
+    per_vs_core_ns = PER_VS_CORE_NS[model_idx]
     est_s = n * sim_steps * per_vs_core_ns * 1e-9 / cores * reps
     # the full workload when it is cheap, else N' = max(64 x cores, 4096) variants
     n_s = n if est_s <= 30.0 else min(n, max(64 * cores, 4096))
@@ -165,6 +170,26 @@ def cpu_reference_rate(model_idx, n, sim_steps, reps=3):
             "walls_s": walls}
 
 
+def cpu_port_rate(model_idx, n, sim_steps, reps=3):
+    """CpgHinge has no reference implementation: time its defining C oracle
+    (oracle/hb_oracle.c, one pthread per host core) instead — kind "port"."""
+    import oracle as O
+    cores = os.cpu_count() or 1
+    est_s = n * sim_steps * PER_VS_CORE_NS[model_idx] * 1e-9 / cores * reps
+    n_s = n if est_s <= 30.0 else min(n, max(64 * cores, 4096))
+    seeds = np.arange(n_s, dtype=np.uint64)
+    walls = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.simulate_batch(model_idx, seeds, sim_steps, cores)
+        walls.append(time.perf_counter() - t0)
+    return {"value": n_s * sim_steps / min(walls), "unit": "variant-steps/s", "cores": cores,
+            "kind": "port",
+            "sample": f"{MODELS[model_idx]} {n_s} variants x {sim_steps} steps through the model's "
+                      f"defining C oracle ({cores} threads; the reference has no such model), best of {reps}",
+            "walls_s": walls}
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(a, ws, rank):
     if rank != 0:
@@ -176,6 +201,11 @@ def run_reference(a, ws, rank):
             "data": "synthetic (seeds 0..N-1, build_model initial states)",
             "config": {"workload": workload_name(a), "model": a.model,
                        "variants_per_gpu": a.variants, "sim_steps": a.sim_steps}}
+    if k == 4:
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "cpg_hinge is not a reference model (SPEC.md:101); "
+                                         "its cpu_baseline is the defining oracle port"}))
+        return
     if not O.ref_available():
         print(json.dumps({"impl": "reference",
                           "unavailable": "oracle/_ref/libhetbench_ref.so was not built"}))
@@ -183,7 +213,7 @@ def run_reference(a, ws, rank):
     cores = O.ref_hardware_concurrency()
     if a.workload == "ea":
         # the reference's own run_ea over cpu_executor(workers = all threads)
-        per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[k]
+        per_vs_core_ns = PER_VS_CORE_NS[k]
         G = a.generations
         pop = a.population
         budget = 10.0 * cores / (per_vs_core_ns * 1e-9) / a.sim_steps  # variants per step
@@ -211,7 +241,7 @@ def run_reference(a, ws, rank):
         return
     n_total = a.variants * a.gpus
     # bounded per-step sample: ~10 s of host time per step at most
-    per_vs_core_ns = {0: 58, 1: 298, 2: 2110, 3: 8190}[k]
+    per_vs_core_ns = PER_VS_CORE_NS[k]
     max_vs = 10.0 * cores / (per_vs_core_ns * 1e-9)
     n_s = n_total if n_total * a.sim_steps <= max_vs else max(64 * cores, int(max_vs // a.sim_steps))
     n_s = min(n_s, n_total)
@@ -332,7 +362,8 @@ def run_ours(a, ws, rank, local):
             "kernel_ms_mean": float(np.mean(kernel_ms)),
             "exact_step_replays": replays,
             "hbm_bytes_per_launch_algorithmic":
-                n * ((0 if a.model == "box" else 8 * (6 * BODIES[a.model] + CONS[a.model]))
+                n * ((0 if a.model == "box" else
+                      8 * (6 * BODIES[a.model] + CONS[a.model] + EXTRA_ROWS.get(a.model, 0)))
                      + 8 + 32 + 8)}
 
     # ---- e2e through the drop-in call (host seeds -> host results) ----
@@ -356,6 +387,7 @@ def run_ours(a, ws, rank, local):
         t_e2e = max_over_ranks(t_e2e)
         assert np.array_equal(r.results, out)
         rows = 6 * BODIES[a.model] + CONS[a.model]
+        rows += EXTRA_ROWS.get(a.model, 0)
         init_bytes = 0 if a.model == "box" else 8 * rows  # Box initial state is built on the device
         e2e = {"value": units * a.steps / t_e2e, "unit": "variant-steps/s",
                "h2d_bytes_per_step": n_total * (8 + init_bytes),

@@ -23,10 +23,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "libhboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libhetbench_ref.so")
 
-BOX, BOX_AND_BALL, ARM_WITH_ROPE, HUMANOID = 0, 1, 2, 3
-MODEL_NAMES = ("box", "box_and_ball", "arm_with_rope", "humanoid")
-BODIES = (1, 2, 12, 32)
-CONSTRAINTS = (0, 1, 11, 46)
+BOX, BOX_AND_BALL, ARM_WITH_ROPE, HUMANOID, CPG_HINGE = 0, 1, 2, 3, 4
+MODEL_NAMES = ("box", "box_and_ball", "arm_with_rope", "humanoid", "cpg_hinge")
+BODIES = (1, 2, 12, 32, 9)
+CONSTRAINTS = (0, 1, 11, 46, 12)
 DT = 0.002
 
 RESULT_DTYPE = np.dtype([("seed", "<u8"), ("fitness", "<f8"), ("checksum", "<u8"),
@@ -82,6 +82,8 @@ def lib():
         L.hbo_time_after.argtypes = [u64, dbl]
         L.hbo_blowup_message.argtypes = [u64, u64, dbl, C.c_char_p, sz]
         L.hbo_run_ea.argtypes = [i32, sz, u64, u64, u64, i32, p(u64), p(dbl)]
+        L.hbo_cpg_build.argtypes = [u64, p(dbl), p(dbl), p(dbl), p(dbl)]
+        L.hbo_cpg_step.argtypes = [p(dbl), p(dbl), p(dbl), p(dbl), dbl, p(dbl)]
     return _orc
 
 
@@ -135,6 +137,20 @@ def build_model(kind: int, seed: int):
     pos = np.zeros((n, 3)); vel = np.zeros((n, 3)); rest = np.zeros(max(m, 1))
     lib().hbo_build_model(kind, seed, _dp(pos), _dp(vel), _dp(rest))
     return pos, vel, rest[:m]
+
+
+def cpg_build(seed: int):
+    """CpgHinge initial state (not in the reference): pos (9,3), vel (9,3),
+    rest (12,) with L0 in 8..11, cpg (16,) = x[4], y[4], omega[4], coupling[4]."""
+    pos = np.zeros((9, 3)); vel = np.zeros((9, 3)); rest = np.zeros(12); cpg = np.zeros(16)
+    lib().hbo_cpg_build(seed, _dp(pos), _dp(vel), _dp(rest), _dp(cpg))
+    return pos, vel, rest, cpg
+
+
+def cpg_step(pos, vel, rest, cpg, dt: float = DT, time: float = 0.0):
+    t = C.c_double(time)
+    rc = lib().hbo_cpg_step(_dp(pos), _dp(vel), _dp(rest), _dp(cpg), dt, C.byref(t))
+    return rc, t.value
 
 
 def step(kind: int, pos, vel, rest, dt: float = DT, time: float = 0.0):

@@ -57,6 +57,7 @@ int hbo_body_count(int kind) {
         case HBO_BOX_AND_BALL: return 2;
         case HBO_ARM_WITH_ROPE: return 12;
         case HBO_HUMANOID: return 32;
+        case HBO_CPG_HINGE: return 9;
     }
     return 0;
 }
@@ -67,6 +68,7 @@ int hbo_constraint_count(int kind) {
         case HBO_BOX_AND_BALL: return 1;
         case HBO_ARM_WITH_ROPE: return 11;
         case HBO_HUMANOID: return 46;
+        case HBO_CPG_HINGE: return 12;
     }
     return 0;
 }
@@ -92,11 +94,19 @@ static void topology(int kind, int* ca, int* cb, double* stiff) {
             for (int i = 16; i < 31; ++i) { ca[m] = i; cb[m] = i + 1; stiff[m++] = kStiffLink; }
             for (int i = 0; i < 16; ++i) { ca[m] = i; cb[m] = 16 + i; stiff[m++] = kStiffLink; }
             break;
+        case HBO_CPG_HINGE:
+            /* NOT IN THE REFERENCE — see cpg section below. */
+            for (int l = 0; l < 4; ++l) {
+                ca[m] = 0; cb[m] = 1 + 2 * l; stiff[m++] = kStiffLink;          /* core - hinge */
+                ca[m] = 1 + 2 * l; cb[m] = 2 + 2 * l; stiff[m++] = kStiffLink;  /* hinge - tip */
+            }
+            for (int l = 0; l < 4; ++l) { ca[m] = 0; cb[m] = 2 + 2 * l; stiff[m++] = kSoftLink; }
+            break;
     }
 }
 
 int hbo_topology(int kind, int* ca, int* cb, double* stiff) {
-    if (kind < 0 || kind > 3) return -1;
+    if (kind < 0 || kind > 4) return -1;
     topology(kind, ca, cb, stiff);
     return hbo_constraint_count(kind);
 }
@@ -110,7 +120,13 @@ static double dist3(const double* p, int a, int b) {
 }
 
 /* build_model  simkernel.cpp:59-120.  pos/vel: AoS [body][xyz]; rest: [m]. */
+int hbo_cpg_build(uint64_t seed, double* pos, double* vel, double* rest, double* cpg);
+
 int hbo_build_model(int kind, uint64_t seed, double* pos, double* vel, double* rest) {
+    if (kind == HBO_CPG_HINGE) {
+        double cpg[16];
+        return hbo_cpg_build(seed, pos, vel, rest, cpg);
+    }
     if (kind < 0 || kind > 3) return -1;
     stream_t rs = {seed, 0};
     const double drop_height = s_range(&rs, 0.5, 2.0);
@@ -233,7 +249,10 @@ uint64_t hbo_checksum(int n, const double* pos, const double* vel) {
 
 /* simulate  simkernel.cpp:187-203.  Returns 0 ok, 1 blow-up (fail_step =
  * number of steps executed incl. the failing one), -1 invalid argument. */
+int hbo_cpg_simulate(uint64_t seed, uint64_t steps, hbo_result* out, uint64_t* fail_step);
+
 int hbo_simulate(int kind, uint64_t seed, uint64_t steps, hbo_result* out, uint64_t* fail_step) {
+    if (kind == HBO_CPG_HINGE) return hbo_cpg_simulate(seed, steps, out, fail_step);
     if (steps < 1 || kind < 0 || kind > 3) return -1;
     double pos[96], vel[96], rest[46];
     hbo_build_model(kind, seed, pos, vel, rest);
@@ -294,7 +313,7 @@ static void* run_job(void* p) {
 
 int hbo_simulate_batch(int kind, const uint64_t* seeds, size_t n, uint64_t steps, int threads,
                        hbo_result* out, uint64_t* fail_step) {
-    if (steps < 1 || n == 0 || kind < 0 || kind > 3) return -1;
+    if (steps < 1 || n == 0 || kind < 0 || kind > 4) return -1;
     if (threads < 1) threads = 1;
     if ((size_t)threads > n) threads = (int)n;
     pthread_t tid[256];
@@ -398,4 +417,117 @@ int hbo_run_ea(int kind, size_t pop, uint64_t generations, uint64_t steps, uint6
     }
     free(res); free(fail); free(order); free(par); free(pfit);
     return rc;
+}
+
+/* ===========================================================================
+ * CPG / hinge modular robot (kind 4) — NOT IN THE REFERENCE.
+ *
+ * BASELINE config 3 names a "Revolve2-style modular robot with hinge joints +
+ * CPG controller"; the reference has none ("joint torque actuation,
+ * controller evolution" are non-goals).  This is its
+ * definition, in simkernel style; the CUDA path is
+ * checked against THIS restatement, so its parity is unpinned by the
+ * reference.
+ *
+ * Bodies (9): core 0; limb l = 0..3 at angle a_l = heading + l*RN(pi/2):
+ *   hinge 1+2l at 0.25 m along a_l, 0.10 m above the core;
+ *   tip   2+2l at 0.50 m along a_l, 0.05 m above the core;
+ *   jitter and launch velocity exactly as build_model (simkernel.cpp:59-92).
+ * Constraints (12, list order): core-hinge, hinge-tip (stiff) per limb,
+ *   then the four actuated core-tip "hinges" (soft) whose rest length is
+ *   L0_l * (1 + 0.2 * u_l), L0_l the initial distance.
+ * CPG per joint l: state (x_l, y_l), parameters omega_l = 2pi * U[0.5, 2),
+ *   c_l = U[-0.5, 0.5) (coupling to joint (l+1) & 3), x_l(0) = U[-0.1, 0.1),
+ *   y_l(0) = 0, drawn from RngStream(seed ^ kCpgKey) in that order.
+ * Step: CPG first (symplectic Euler on the old state),
+ *     nx_l = x_l + dt * (omega_l * y_l + c_l * x_{(l+1)&3})
+ *     y_l  = y_l - dt * (omega_l * nx_l);  x_l = nx_l
+ *     u_l  = clamp(x_l, -1, 1)
+ *   then the reference step() with the updated rest lengths.
+ * Checksum: FNV-1a over positions, velocities, then x[4], y[4].
+ * Known answer: omega = c = x(0) = 0 keeps every rest length at L0 exactly,
+ * i.e. the passive robot.
+ * ======================================================================== */
+static const uint64_t kCpgKey = 0xC0FFEE5EEDC0DE5Full;
+
+int hbo_cpg_build(uint64_t seed, double* pos, double* vel, double* rest, double* cpg) {
+    stream_t rs = {seed, 0};
+    const double drop_height = s_range(&rs, 0.5, 2.0);
+    const double lx = s_range(&rs, -1.0, 1.0);
+    const double ly = s_range(&rs, -1.0, 1.0);
+    const double heading = s_range(&rs, 0.0, 2.0 * 3.14159265358979323846);
+    for (int i = 0; i < 9; ++i) {
+        double x, y, z;
+        if (i == 0) {
+            x = 0.0; y = 0.0; z = drop_height;
+        } else {
+            const int l = (i - 1) / 2;
+            const int tip = (i - 1) % 2;
+            const double a = heading + 1.5707963267948966 * (double)l;
+            const double r = tip ? 0.50 : 0.25;
+            x = r * cos(a);
+            y = r * sin(a);
+            z = drop_height + (tip ? 0.05 : 0.10);
+        }
+        x += 1e-3 * s_range(&rs, -1.0, 1.0);
+        y += 1e-3 * s_range(&rs, -1.0, 1.0);
+        z += 1e-3 * s_unit(&rs);
+        pos[3 * i + 0] = x; pos[3 * i + 1] = y; pos[3 * i + 2] = z;
+        vel[3 * i + 0] = lx; vel[3 * i + 1] = ly; vel[3 * i + 2] = 0.0;
+    }
+    int ca[12], cb[12];
+    double st[12];
+    topology(HBO_CPG_HINGE, ca, cb, st);
+    for (int k = 0; k < 12; ++k) rest[k] = dist3(pos, ca[k], cb[k]);
+    stream_t cs = {seed ^ kCpgKey, 0};
+    for (int l = 0; l < 4; ++l) cpg[8 + l] = (2.0 * 3.14159265358979323846) * s_range(&cs, 0.5, 2.0);
+    for (int l = 0; l < 4; ++l) cpg[12 + l] = s_range(&cs, -0.5, 0.5);
+    for (int l = 0; l < 4; ++l) cpg[l] = s_range(&cs, -0.1, 0.1);
+    for (int l = 0; l < 4; ++l) cpg[4 + l] = 0.0;
+    return 0;
+}
+
+/* One CPG step + physics step.  rest_base[12] holds the static rests and
+ * L0 (indices 8..11); cpg = {x[4], y[4], omega[4], c[4]} updated in place. */
+int hbo_cpg_step(double* pos, double* vel, const double* rest_base, double* cpg, double dt,
+                 double* time) {
+    if (!(dt > 0.0)) return -1;
+    double nx[4];
+    for (int l = 0; l < 4; ++l)
+        nx[l] = cpg[l] + dt * (cpg[8 + l] * cpg[4 + l] + cpg[12 + l] * cpg[(l + 1) & 3]);
+    for (int l = 0; l < 4; ++l) {
+        cpg[4 + l] = cpg[4 + l] - dt * (cpg[8 + l] * nx[l]);
+        cpg[l] = nx[l];
+    }
+    double rest[12];
+    for (int k = 0; k < 8; ++k) rest[k] = rest_base[k];
+    for (int l = 0; l < 4; ++l) {
+        const double x = cpg[l];
+        const double u = (x < -1.0) ? -1.0 : ((x > 1.0) ? 1.0 : x);
+        rest[8 + l] = rest_base[8 + l] * (1.0 + 0.2 * u);
+    }
+    return hbo_step(HBO_CPG_HINGE, pos, vel, rest, dt, time);
+}
+
+int hbo_cpg_simulate(uint64_t seed, uint64_t steps, hbo_result* out, uint64_t* fail_step) {
+    if (steps < 1) return -1;
+    double pos[27], vel[27], rest[12], cpg[16];
+    hbo_cpg_build(seed, pos, vel, rest, cpg);
+    const double sx = pos[0], sy = pos[1];
+    double time = 0.0;
+    for (uint64_t s = 0; s < steps; ++s) {
+        if (hbo_cpg_step(pos, vel, rest, cpg, 0.002, &time) == 1) {
+            if (fail_step) *fail_step = s + 1;
+            return 1;
+        }
+    }
+    const double dx = pos[0] - sx, dy = pos[1] - sy;
+    uint64_t h = hbo_checksum(9, pos, vel);
+    for (int l = 0; l < 8; ++l) h = fnv_absorb(h, cpg[l]);
+    out->seed = seed;
+    out->fitness = sqrt(dx * dx + dy * dy);
+    out->checksum = h;
+    out->steps_executed = steps;
+    if (fail_step) *fail_step = 0;
+    return 0;
 }

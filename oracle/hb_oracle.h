@@ -9,7 +9,7 @@
 extern "C" {
 #endif
 
-enum { HBO_BOX = 0, HBO_BOX_AND_BALL = 1, HBO_ARM_WITH_ROPE = 2, HBO_HUMANOID = 3 };
+enum { HBO_BOX = 0, HBO_BOX_AND_BALL = 1, HBO_ARM_WITH_ROPE = 2, HBO_HUMANOID = 3, HBO_CPG_HINGE = 4 };
 
 /* Layout-identical to hetbench::VariantResult (simkernel.hpp:51-58). */
 typedef struct {
@@ -44,6 +44,11 @@ int hbo_plan_allocation(double t_cpu, double t_accel, int cpu_ok, int accel_ok, 
 void hbo_stable_order_desc(const double* fitness, size_t n, size_t* order);
 uint64_t hbo_init_genome(uint64_t seed, uint64_t i);
 uint64_t hbo_child_genome(uint64_t parent, uint64_t g, uint64_t i);
+/* CPG / hinge model (kind 4, not in the reference; see hb_oracle.c). */
+int hbo_cpg_build(uint64_t seed, double* pos, double* vel, double* rest, double* cpg);
+int hbo_cpg_step(double* pos, double* vel, const double* rest_base, double* cpg, double dt,
+                 double* time);
+int hbo_cpg_simulate(uint64_t seed, uint64_t steps, hbo_result* out, uint64_t* fail_step);
 int hbo_run_ea(int kind, size_t pop, uint64_t generations, uint64_t steps, uint64_t seed,
                int threads, uint64_t* genomes, double* fitness);
 

@@ -29,20 +29,41 @@ constexpr double kStiffLink = 2.5e5;
 constexpr double kSoftLink = 1.25e5;
 constexpr double kMinDist = 1e-12;  // simkernel.cpp:144
 
-enum Kind : int { Box = 0, BoxAndBall = 1, ArmWithRope = 2, Humanoid = 3 };
+// Kinds 0-3 are hetbench::ModelKind (simkernel.hpp:14).  Kind 4 (CpgHinge)
+// is NOT in the reference: the "Revolve2-style modular robot with hinge
+// joints + CPG controller" of BASELINE config 3, defined in
+// oracle/hb_oracle.c (its oracle) and DESIGN.md §3.6.
+enum Kind : int { Box = 0, BoxAndBall = 1, ArmWithRope = 2, Humanoid = 3, CpgHinge = 4 };
+constexpr int kNumKinds = 5;
 
-HB_HD constexpr int bodies(int k) { return k == 0 ? 1 : k == 1 ? 2 : k == 2 ? 12 : k == 3 ? 32 : 0; }
-HB_HD constexpr int constraints(int k) { return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 11 : k == 3 ? 46 : 0; }
-HB_HD constexpr int state_rows(int k) { return 6 * bodies(k) + constraints(k); }
+HB_HD constexpr int bodies(int k) {
+    return k == 0 ? 1 : k == 1 ? 2 : k == 2 ? 12 : k == 3 ? 32 : k == 4 ? 9 : 0;
+}
+HB_HD constexpr int constraints(int k) {
+    return k == 0 ? 0 : k == 1 ? 1 : k == 2 ? 11 : k == 3 ? 46 : k == 4 ? 12 : 0;
+}
+// CPG rows of kind 4: x[4], y[4], omega[4], coupling[4].
+HB_HD constexpr int cpg_rows(int k) { return k == 4 ? 16 : 0; }
+HB_HD constexpr int state_rows(int k) { return 6 * bodies(k) + constraints(k) + cpg_rows(k); }
 
 // Constraint c of model k: endpoints (a, b) and whether it is a soft link.
+// Kind 4: c = 2l core-hinge (0, 1+2l), c = 2l+1 hinge-tip (1+2l, 2+2l),
+// c = 8+l actuated core-tip (0, 2+2l, soft).
 HB_HD constexpr int con_a(int k, int c) {
-    return k == 3 ? (c < 15 ? c : c < 30 ? c + 1 : c - 30) : c;
+    return k == 3 ? (c < 15 ? c : c < 30 ? c + 1 : c - 30)
+         : k == 4 ? (c < 8 ? (c % 2 == 0 ? 0 : c) : 0)
+                  : c;
 }
 HB_HD constexpr int con_b(int k, int c) {
-    return k == 3 ? (c < 15 ? c + 1 : c < 30 ? c + 2 : c - 30 + 16) : c + 1;
+    return k == 3 ? (c < 15 ? c + 1 : c < 30 ? c + 2 : c - 30 + 16)
+         : k == 4 ? (c < 8 ? c + 1 : 2 * c - 14)
+                  : c + 1;
 }
-HB_HD constexpr bool con_soft(int k, int c) { return k == 2 && c >= 5; }
+HB_HD constexpr bool con_soft(int k, int c) { return (k == 2 && c >= 5) || (k == 4 && c >= 8); }
+HB_HD constexpr bool is_chain(int k) { return k == 1 || k == 2; }
+
+constexpr uint64_t kCpgKey = 0xC0FFEE5EEDC0DE5Full;
+constexpr double kCpgAmp = 0.2;
 
 // ---- counter-based generator (rng.hpp:15-32) ----
 HB_HD constexpr uint64_t mix64(uint64_t x) {

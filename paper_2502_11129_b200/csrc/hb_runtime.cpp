@@ -40,7 +40,7 @@ hb_status set_global(hb_status st, const std::string& msg) {
     return st;
 }
 
-bool valid_kind(int kind) { return kind >= 0 && kind <= 3; }
+bool valid_kind(int kind) { return kind >= 0 && kind < hb::kNumKinds; }
 
 // ---------------------------------------------------------------------------
 // Persistent fork/join pool.  The caller thread takes part; work is handed
@@ -189,8 +189,57 @@ void build_one(uint64_t seed, double* soa, size_t ld, size_t i) {
     }
 }
 
+// CpgHinge (kind 4, not in the reference; definition: oracle/hb_oracle.c
+// hbo_cpg_build): core + four 2-module limbs, plus the CPG rows
+// x[4], y[4], omega[4], coupling[4] after the 12 rest rows.
+void build_cpg(uint64_t seed, double* soa, size_t ld, size_t i) {
+    constexpr int n = 9, m = 12;
+    Stream rs{seed, 0};
+    const double drop_height = rs.range(0.5, 2.0);
+    const double lx = rs.range(-1.0, 1.0);
+    const double ly = rs.range(-1.0, 1.0);
+    const double heading = rs.range(0.0, 2.0 * 3.14159265358979323846);
+    double px[n], py[n], pz[n];
+    for (int b = 0; b < n; ++b) {
+        double x, y, z;
+        if (b == 0) {
+            x = 0.0; y = 0.0; z = drop_height;
+        } else {
+            const int l = (b - 1) / 2;
+            const bool tip = ((b - 1) % 2) != 0;
+            const double a = heading + 1.5707963267948966 * static_cast<double>(l);
+            const double r = tip ? 0.50 : 0.25;
+            x = r * std::cos(a);
+            y = r * std::sin(a);
+            z = drop_height + (tip ? 0.05 : 0.10);
+        }
+        x += 1e-3 * rs.range(-1.0, 1.0);
+        y += 1e-3 * rs.range(-1.0, 1.0);
+        z += 1e-3 * rs.unit();
+        px[b] = x; py[b] = y; pz[b] = z;
+        soa[(3 * b + 0) * ld + i] = x;
+        soa[(3 * b + 1) * ld + i] = y;
+        soa[(3 * b + 2) * ld + i] = z;
+        soa[(3 * n + 3 * b + 0) * ld + i] = lx;
+        soa[(3 * n + 3 * b + 1) * ld + i] = ly;
+        soa[(3 * n + 3 * b + 2) * ld + i] = 0.0;
+    }
+    for (int c = 0; c < m; ++c) {
+        const int A = hb::con_a(4, c), B = hb::con_b(4, c);
+        const double dx = px[B] - px[A], dy = py[B] - py[A], dz = pz[B] - pz[A];
+        soa[(6 * n + c) * ld + i] = std::sqrt(dx * dx + dy * dy + dz * dz);
+    }
+    Stream cs{seed ^ hb::kCpgKey, 0};
+    double* cpg = soa + (6 * n + m) * ld + i;  // row r at cpg[r * ld]
+    for (int l = 0; l < 4; ++l) cpg[(8 + l) * ld] = (2.0 * 3.14159265358979323846) * cs.range(0.5, 2.0);
+    for (int l = 0; l < 4; ++l) cpg[(12 + l) * ld] = cs.range(-0.5, 0.5);
+    for (int l = 0; l < 4; ++l) cpg[l * ld] = cs.range(-0.1, 0.1);
+    for (int l = 0; l < 4; ++l) cpg[(4 + l) * ld] = 0.0;
+}
+
 void build_range(int kind, const uint64_t* seeds, size_t b, size_t e, double* soa, size_t ld) {
     switch (kind) {
+        case 4: for (size_t i = b; i < e; ++i) build_cpg(seeds[i], soa, ld, i); break;
         case 0: for (size_t i = b; i < e; ++i) build_one<0>(seeds[i], soa, ld, i); break;
         case 1: for (size_t i = b; i < e; ++i) build_one<1>(seeds[i], soa, ld, i); break;
         case 2: for (size_t i = b; i < e; ++i) build_one<2>(seeds[i], soa, ld, i); break;

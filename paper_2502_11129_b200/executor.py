@@ -24,14 +24,19 @@ KSIM_DT = 0.002
 
 
 class ModelKind(enum.IntEnum):
-    """hetbench::ModelKind (simkernel.hpp:14), same ordinals."""
+    """hetbench::ModelKind (simkernel.hpp:14), same ordinals; CpgHinge (4) is
+    the CPG / hinge modular robot of BASELINE config 3, which the reference
+    does not have — defined by oracle/hb_oracle.c, parity
+    against that definition only."""
     Box = 0
     BoxAndBall = 1
     ArmWithRope = 2
     Humanoid = 3
+    CpgHinge = 4
 
 
-_NAMES = ("box", "box_and_ball", "arm_with_rope", "humanoid")
+_NAMES = ("box", "box_and_ball", "arm_with_rope", "humanoid", "cpg_hinge")
+REFERENCE_MODELS = (ModelKind.Box, ModelKind.BoxAndBall, ModelKind.ArmWithRope, ModelKind.Humanoid)
 ALL_MODELS = tuple(ModelKind)
 
 
@@ -245,15 +250,19 @@ class GpuExecutor(BatchExecutor):
         return BatchResult(out, wall, [])
 
     def run_states(self, kind: ModelKind, pos: np.ndarray, vel: np.ndarray, rest: np.ndarray,
-                   steps: int = 1, dt: float = KSIM_DT, seeds=None):
+                   steps: int = 1, dt: float = KSIM_DT, seeds=None, cpg=None):
         """Run from explicit initial states (known-answer tests).  pos/vel:
-        (N, n, 3); rest: (N, m).  Returns (results, fail_step, pos, vel)."""
+        (N, n, 3); rest: (N, m); cpg (CpgHinge only): (N, 16) = x[4], y[4],
+        omega[4], coupling[4].  Returns (results, fail_step, pos, vel)."""
         pos = np.asarray(pos, dtype=np.float64)
         vel = np.asarray(vel, dtype=np.float64)
         N, nb = pos.shape[0], pos.shape[1]
         m = constraint_count(kind)
         rest = np.asarray(rest, dtype=np.float64).reshape(N, m)
-        soa = np.concatenate([pos.reshape(N, 3 * nb).T, vel.reshape(N, 3 * nb).T, rest.T], axis=0)
+        parts = [pos.reshape(N, 3 * nb).T, vel.reshape(N, 3 * nb).T, rest.T]
+        if int(kind) == int(ModelKind.CpgHinge):
+            parts.append(np.asarray(cpg, dtype=np.float64).reshape(N, 16).T)
+        soa = np.concatenate(parts, axis=0)
         soa = np.ascontiguousarray(soa)
         final = np.empty_like(soa)
         out = np.empty(N, dtype=RESULT_DTYPE)

@@ -150,6 +150,21 @@ def main():
         json.dump(g, f, indent=0, sort_keys=True)
     print("wrote", path, os.path.getsize(path), "bytes")
 
+    # CpgHinge (kind 4) is NOT in the reference: its values come from the
+    # oracle that defines it (oracle/hb_oracle.c) — a regression anchor only.
+    cg = {"source": "oracle/_build/libhboracle.so (model defined there; parity unpinned)",
+          "simulate": []}
+    for seed in (0, 1, 42, 2**64 - 1):
+        for steps in (1, 10, 1000, 5000):
+            rc, r, _ = O.simulate(4, seed, steps)
+            assert rc == 0
+            cg["simulate"].append({"seed": str(seed), "steps": steps, "fitness_bits": fbits(r[1]),
+                                   "checksum": hx(r[2])})
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpg_golden.json")
+    with open(path, "w") as f:
+        json.dump(cg, f, indent=0, sort_keys=True)
+    print("wrote", path)
+
 
 if __name__ == "__main__":
     main()

