@@ -104,7 +104,13 @@ hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 #define HB_KERNEL_GENERIC 1
 hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 
-/* Page-locked host memory (cudaHostAlloc, portable).  hb_run_batch / hb_fetch
+/* Zero-copy Box path (default on): when a Box batch's seeds and `out` are both
+ * mapped page-locked memory (e.g. hb_host_alloc), the kernel reads the seeds
+ * and writes the results through the host mapping — no H2D / D2H operation
+ * on the call's critical path.  0 disables it (always stage + DMA). */
+hb_status hb_ctx_set_zero_copy(hb_ctx* ctx, int enable);
+
+/* Page-locked host memory (cudaHostAlloc, portable + mapped).  hb_run_batch / hb_fetch
  * DMA the results straight into an `out` buffer allocated here (no staging
  * copy); any other buffer goes through the context's staging buffer. */
 void* hb_host_alloc(size_t bytes);

@@ -8,7 +8,8 @@ contract.  Native code: libhbgpu.so (csrc/, C ABI in include/hbgpu.h).
 from .executor import (ALL_MODELS, BatchExecutor, BatchFailure, BatchRequest, BatchResult,
                        DeviceContext, GpuExecutor, ModelKind, MultiGpuExecutor, NumericalBlowup,
                        RESULT_DTYPE, body_count, build_states, constraint_count, device_count,
-                       format_blowup, kernel_name, parse_model_kind, state_rows, to_string,
+                       format_blowup, kernel_name, parse_model_kind, pinned_seeds, state_rows,
+                       to_string,
                        validate_request)
 from .scheduler import (AllocationPlan, CalibrationProfile, HybridResult, calibrate, calibrate_n,
                         format_plan, naive_sum, plan_allocation, plan_allocation_n,

@@ -29,6 +29,9 @@ struct SimArgs {
     uint64_t* fail;
     unsigned* counters;
     double* final_state;
+    // nullable: host-mapped flag a failing variant sets to 1 (plain store;
+    // lets a zero-copy launch report "something blew up" without a D2H)
+    volatile unsigned* fail_flag;
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);

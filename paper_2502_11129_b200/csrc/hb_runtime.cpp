@@ -301,6 +301,7 @@ struct hb_ctx {
     uint64_t last_replays = 0;
     size_t last_n = 0;
     bool counters_dirty = true;  // device counters need a reset before the next launch
+    bool zero_copy = true;       // Box: read seeds / write results through host mappings
 
     hb_status fail(hb_status st, const std::string& msg) {
         err = msg;
@@ -389,6 +390,17 @@ bool init_on_device(const hb_ctx* c, int kind) {
 
 constexpr size_t kParallelCopyMin = 2048;  // min items per host thread for copies / assembly
 
+// Device address of page-locked, mapped host memory (nullptr if `p` is not).
+void* mapped_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (at.type != cudaMemoryTypeHost) return nullptr;
+    return at.devicePointer;
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -466,7 +478,7 @@ hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool 
         c->counters_dirty = false;
     }
     hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
-                  c->d_out, c->d_fail, c->d_count, d_final};
+                  c->d_out, c->d_fail, c->d_count, d_final, nullptr};
     c->last_steps = steps;
     return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch");
 }
@@ -562,7 +574,7 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_scratch, 64) != cudaSuccess ||
         cudaMalloc(&c->d_count, 16) != cudaSuccess ||
-        cudaHostAlloc(&c->h_count, 16, 0) != cudaSuccess) {
+        cudaHostAlloc(&c->h_count, 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
         delete c;
         return set_global(HB_CUDA_ERROR, "stream/scratch creation failed");
     }
@@ -597,7 +609,8 @@ hb_status hb_ctx_set_host_threads(hb_ctx* c, int threads) {
 
 void* hb_host_alloc(size_t bytes) {
     void* p = nullptr;
-    if (bytes == 0 || cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    if (bytes == 0 ||
+        cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
         cudaGetLastError();
         set_global(HB_CUDA_ERROR, "cudaHostAlloc failed");
         return nullptr;
@@ -624,6 +637,12 @@ hb_status hb_last_launch_stats(hb_ctx* c, uint64_t* failed, uint64_t* exact_repl
     return HB_OK;
 }
 
+hb_status hb_ctx_set_zero_copy(hb_ctx* c, int enable) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    c->zero_copy = enable != 0;
+    return HB_OK;
+}
+
 hb_status hb_ctx_set_kernel(hb_ctx* c, int variant) {
     if (!c || (variant != HB_KERNEL_AUTO && variant != HB_KERNEL_GENERIC))
         return set_global(HB_INVALID_ARG, "bad kernel variant");
@@ -639,10 +658,65 @@ hb_status hb_build_states(int kind, const uint64_t* seeds, size_t n, double* soa
     return HB_OK;
 }
 
+// Box with seeds and results both in mapped page-locked memory: the kernel
+// reads the seeds and writes the 32-byte results through the host mapping
+// (zero-copy) — no H2D / D2H operations on the call's critical path; a
+// host-mapped flag tells whether anything blew up.
+static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant_result* dout, size_t n,
+                            uint64_t steps, hb_variant_result* out, uint64_t* fail_step, bool* any) {
+    Trace tr("zero-copy");
+    HB_TRY(ensure_capacity(c, hb::Box, n, false));
+    if (c->counters_dirty) {
+        HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
+        c->counters_dirty = false;
+    }
+    volatile unsigned* flag = reinterpret_cast<volatile unsigned*>(c->h_count + 2);
+    *flag = 0u;
+    void* dflag = mapped_device_ptr(c->h_count);
+    hb::SimArgs a{nullptr, dseeds, n, n, steps, hb::kSimDt, dout, c->d_fail, c->d_count, nullptr,
+                  reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2)};
+    c->staged_kind = -1;
+    HB_TRY(c->cuda(hb::launch_sim(hb::Box, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
+    tr.mark("launch");
+    HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+    tr.mark("sync");
+    c->last_n = n;
+    c->last_replays = 0;
+    *any = *flag != 0u;
+    if (*any) {
+        HB_TRY(c->cuda(cudaMemcpy(c->h_fail, c->d_fail, n * sizeof(uint64_t), cudaMemcpyDeviceToHost),
+                       "D2H fail"));
+        c->last_failed = 0;
+        for (size_t i = 0; i < n; ++i) c->last_failed += c->h_fail[i] != 0;
+        c->counters_dirty = true;
+    } else {
+        c->last_failed = 0;
+    }
+    if (fail_step) {
+        if (*any) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
+        else std::memset(fail_step, 0, n * sizeof(uint64_t));
+    }
+    (void)out;
+    return HB_OK;
+}
+
 hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
                        hb_variant_result* out, uint64_t* fail_step, double* wall_time_s) {
     const auto t0 = std::chrono::steady_clock::now();
     HB_TRY(validate(c, kind, seeds, n, steps, out));
+    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO && c->zero_copy) {
+        void* ds = mapped_device_ptr(seeds);
+        void* dout = mapped_device_ptr(out);
+        if (ds && dout) {
+            bool any = false;
+            HB_TRY(run_box_zero_copy(c, static_cast<const uint64_t*>(ds),
+                                     static_cast<hb_variant_result*>(dout), n, steps, out, fail_step,
+                                     &any));
+            if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
+            if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+            return HB_OK;
+        }
+    }
     HB_TRY(stage_inputs(c, kind, seeds, n));
     HB_TRY(launch(c, kind, n, steps, hb::kSimDt, c->staged_from_seeds, nullptr));
     bool any = false;
@@ -947,7 +1021,7 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
         c->counters_dirty = false;
     }
     hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
-                  c->d_out, c->d_fail, c->d_count, nullptr};
+                  c->d_out, c->d_fail, c->d_count, nullptr, nullptr};
     HB_TRY(c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
     HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,

@@ -196,6 +196,10 @@ class DeviceContext:
         self.check(lib.hb_last_launch_stats(self.handle, C.byref(f), C.byref(r)), "stats")
         return int(f.value), int(r.value)
 
+    def set_zero_copy(self, enable: bool) -> None:
+        """Box zero-copy path for pinned seeds + results (default on)."""
+        self.check(lib.hb_ctx_set_zero_copy(self.handle, int(bool(enable))), "hb_ctx_set_zero_copy")
+
     def set_kernel(self, variant: int) -> None:
         """_lib.HB_KERNEL_AUTO (optimised) or _lib.HB_KERNEL_GENERIC (reference-order cross-check)."""
         self.check(lib.hb_ctx_set_kernel(self.handle, int(variant)), "hb_ctx_set_kernel")
@@ -327,6 +331,15 @@ def build_states(kind: ModelKind, seeds) -> np.ndarray:
     if st != _lib.HB_OK:
         raise ValueError(_lib.global_error())
     return soa
+
+
+def pinned_seeds(seeds) -> np.ndarray:
+    """A copy of `seeds` in mapped page-locked memory (recycled pool): H2D
+    without staging, and the Box zero-copy path."""
+    src = np.ascontiguousarray(seeds, dtype=np.uint64)
+    out = _lib.pinned.empty(len(src), np.uint64)
+    out[:] = src
+    return out
 
 
 def kernel_name(kind: ModelKind, n: int) -> str:

@@ -262,3 +262,20 @@ def test_exact_replay_path_blowup_states(gpu, gpu_generic):
     ok = a[1] == 0
     assert np.array_equal(a[0][ok], b[0][ok])
     assert np.array_equal(a[2][ok], b[2][ok]) and np.array_equal(a[3][ok], b[3][ok])
+
+
+def test_box_zero_copy_path_equals_staged(gpu):
+    """Box with pinned seeds + pinned results runs zero-copy (seeds read and
+    results written through the host mapping); results identical to the
+    staged path and the oracle, including a batch size that is not a
+    multiple of any CTA size."""
+    for n, steps in ((16384, 1000), (1000, 777), (1, 5)):
+        seeds = np.arange(n, dtype=np.uint64) * np.uint64(6364136223846793005)
+        ps = hb.pinned_seeds(seeds)
+        a = gpu.run(hb.BatchRequest(0, ps, steps)).results
+        gpu.ctx.set_zero_copy(False)
+        b = gpu.run(hb.BatchRequest(0, ps, steps)).results
+        gpu.ctx.set_zero_copy(True)
+        assert np.array_equal(a, b)
+        sub = slice(0, n, max(1, n // 200))
+        assert np.array_equal(a[sub], O.simulate_batch(0, seeds[sub], steps).results)
