@@ -17,6 +17,8 @@ from .scheduler import (AllocationPlan, CalibrationProfile, HybridResult, calibr
 from .ea import (EaResult, PhaseProfile, Population, report_profile, rng_at, run_ea,
                  run_ea_native, stable_order_desc)
 
+from .monitor import GpuUtilSampler, KneeRegime, Stats, detect_saturation_knee, summarize
+
 LIB_PATH = __import__("paper_2502_11129_b200._lib", fromlist=["LIB_PATH"]).LIB_PATH
 
 __all__ = [n for n in dir() if not n.startswith("_")]

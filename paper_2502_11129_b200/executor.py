@@ -224,8 +224,10 @@ class DeviceContext:
 class GpuExecutor(BatchExecutor):
     """The B200 accelerator back-end: one device, one persistent kernel per batch."""
 
-    def __init__(self, device: int = 0, host_threads: int = 0, kernel: int = _lib.HB_KERNEL_AUTO):
+    def __init__(self, device: int = 0, host_threads: int = 0, kernel: int = _lib.HB_KERNEL_AUTO,
+                 monitor: bool = False):
         self.ctx = DeviceContext(device, host_threads)
+        self.monitor = monitor  # NVML utilisation trace, like cpu_executor(monitor=true)
         if kernel != _lib.HB_KERNEL_AUTO:
             self.ctx.set_kernel(kernel)
 
@@ -248,10 +250,16 @@ class GpuExecutor(BatchExecutor):
 
     def run(self, request: BatchRequest) -> BatchResult:
         validate_request(request)
+        sampler = None
+        if self.monitor:
+            from .monitor import GpuUtilSampler
+            sampler = GpuUtilSampler(self.ctx.device)
+            sampler.start()
         out, fail, wall, st = self.run_raw(request.kind, request.seeds, request.steps)
+        trace = sampler.stop() if sampler is not None else []
         if st == _lib.HB_BLOWUP_PARTIAL:
             _raise_partial(request.seeds, out, fail)
-        return BatchResult(out, wall, [])
+        return BatchResult(out, wall, trace)
 
     def run_states(self, kind: ModelKind, pos: np.ndarray, vel: np.ndarray, rest: np.ndarray,
                    steps: int = 1, dt: float = KSIM_DT, seeds=None, cpg=None):

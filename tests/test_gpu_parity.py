@@ -279,3 +279,35 @@ def test_box_zero_copy_path_equals_staged(gpu):
         assert np.array_equal(a, b)
         sub = slice(0, n, max(1, n // 200))
         assert np.array_equal(a[sub], O.simulate_batch(0, seeds[sub], steps).results)
+
+
+@pytest.mark.parametrize("kind,n,steps,stride", [
+    (4, 8192, 5000, 257),    # configs[2]: CPG / hinge robot, 8192 x 5000
+    (3, 8192, 5000, 509),    # its humanoid proxy
+    (0, 32768, 20000, 997),  # configs[3] endpoint: 32768 x 20000
+    (1, 32768, 20000, 2003),
+    (2, 32768, 2000, 4001),
+])
+def test_baseline_sizes_subsampled_vs_oracle(gpu, kind, n, steps, stride):
+    """BASELINE configs at full size on the GPU; an evenly strided subsample
+    re-simulated by the oracle must match bit for bit, no variant may blow
+    up, and a checksum-of-checksums pins the whole batch for determinism."""
+    seeds = np.arange(n, dtype=np.uint64)
+    res = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+    assert np.all(res["steps_executed"] == steps)
+    sub = slice(0, n, stride)
+    assert np.array_equal(res[sub], O.simulate_batch(kind, seeds[sub], steps).results)
+    again = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+    cc = np.bitwise_xor.reduce(res["checksum"] * np.uint64(0x9E3779B97F4A7C15))
+    assert cc == np.bitwise_xor.reduce(again["checksum"] * np.uint64(0x9E3779B97F4A7C15))
+
+
+def test_nvml_utilisation_trace():
+    """GpuExecutor(monitor=True) fills BatchResult.utilization_trace from NVML
+    (the accelerator side the reference leaves at 0, monitor.cpp:164)."""
+    ex = hb.GpuExecutor(0, monitor=True)
+    res = ex.run(hb.BatchRequest(3, np.arange(16384, dtype=np.uint64), 3000))
+    tr = res.utilization_trace
+    assert len(tr) >= 2
+    assert all(0.0 <= u <= 100.0 for _, u in tr)
+    assert max(u for _, u in tr) > 0.0

@@ -35,14 +35,8 @@ W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240
 
 
 def t_ci95(samples):
-    x = np.asarray(samples, dtype=float)
-    n = len(x)
-    m = float(x.mean())
-    if n < 2:
-        return m, m, m
-    from scipy import stats
-    h = float(stats.t.ppf(0.975, n - 1) * x.std(ddof=1) / np.sqrt(n))
-    return m, m - h, m + h
+    st = hb.summarize(samples)
+    return st.mean, st.ci95_low, st.ci95_high
 
 
 def e2e_walls(ex, kind, n, steps, reps):
@@ -78,19 +72,8 @@ def kernel_ms(ex, kind, n, steps, reps=3):
 
 
 def knee(ns, walls):
-    import ctypes as C
-    import oracle as O
-    if not O.ref_available():
-        return None
-    L = O.ref()
-    n = np.ascontiguousarray(ns, dtype=np.uint64)
-    w = np.ascontiguousarray(walls, dtype=np.float64)
-    kn, reg = C.c_uint64(0), C.c_int(0)
-    if L.hbref_detect_knee(n.ctypes.data_as(C.POINTER(C.c_uint64)),
-                           w.ctypes.data_as(C.POINTER(C.c_double)), len(n), 0.05, C.byref(kn),
-                           C.byref(reg)):
-        return None
-    return {"n": int(kn.value), "regime": ["knee", "all_flat", "all_linear"][reg.value]}
+    n, regime = hb.detect_saturation_knee(list(zip(ns, walls)))
+    return {"n": int(n), "regime": regime.name}
 
 
 def cpu_rate(kind, steps=1000):
