@@ -235,7 +235,8 @@ class GpuExecutor(BatchExecutor):
         return "accel"
 
     def run_raw(self, kind: ModelKind, seeds: np.ndarray, steps: int):
-        """(results, fail_step, wall_s, status) without raising on blow-up."""
+        """(results, fail_step or None, wall_s, status) without raising on
+        blow-up; fail_step is only materialised when something blew up."""
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
         n = len(seeds)
         out = _lib.pinned.empty(n, RESULT_DTYPE)
@@ -243,8 +244,9 @@ class GpuExecutor(BatchExecutor):
         st = lib.hb_run_batch(self.ctx.handle, int(kind), _lib.ptr(seeds), n, int(steps),
                               _lib.ptr(out), None, C.byref(wall))
         self.ctx.check(st, "hb_run_batch")
-        fail = np.zeros(n, dtype=np.uint64)
+        fail = None  # per-variant failure steps only exist after a blow-up
         if st == _lib.HB_BLOWUP_PARTIAL:
+            fail = np.zeros(n, dtype=np.uint64)
             self.ctx.check(lib.hb_last_fail_steps(self.ctx.handle, _lib.ptr(fail), n), "fail steps")
         return out, fail, wall.value, st
 
