@@ -104,6 +104,22 @@ __global__ void lat_sqrt(double* out, double a, long long* cyc) {
     if (threadIdx.x == 0) *cyc = t1 - t0;
 }
 
+// Box grounded-phase step: two independent 5-op chains (x, y) per step.
+__global__ void chain_xy(double* out, double a, long long* cyc) {
+    const double damp = 1.0 - 0.8 * a * 1e-3, dt = a * 2e-3, inv = 1.0 / dt;
+    double px = threadIdx.x, py = 1.0, vx = 0.3, vy = -0.2;
+    long long t0 = clock64();
+#pragma unroll 16
+    for (int i = 0; i < N_ITERS; ++i) {
+        const double qx = px + (vx * damp) * dt, qy = py + (vy * damp) * dt;
+        vx = (qx - px) * inv; vy = (qy - py) * inv;
+        px = qx; py = qy;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = px + py + vx + vy;
+    if (threadIdx.x == 0 && blockIdx.x == 0) *cyc = t1 - t0;
+}
+
 int main() {
     double* out;
     long long* cyc;
@@ -123,6 +139,19 @@ int main() {
         {"DADD 8 warps/SM 8 chains (cyc/warp-instr/SMSP)", thr_dadd, 256, 8.0 * N_ITERS / 2},
         {"DSETP 1 warp 4 chains (cyc/warp-instr)", thr_dsetp, 32, 4.0 * N_ITERS},
     };
+    {
+        // grounded-step chain: 1 CTA, then the full 16384-variant grid (512 x 32)
+        double* big;
+        cudaMalloc(&big, 16384 * sizeof(double));
+        for (int grid : {1, 148, 296, 512, 592, 1184}) {
+            for (int it = 0; it < 2; ++it) { chain_xy<<<grid, 32>>>(big, 1.0, cyc); cudaDeviceSynchronize(); }
+            cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+            cudaEventRecord(e0); chain_xy<<<grid, 32>>>(big, 1.0, cyc); cudaEventRecord(e1); cudaEventSynchronize(e1);
+            float ms; cudaEventElapsedTime(&ms, e0, e1);
+            printf("chain_xy grid %4d x 32: %6.2f cyc/step (clock64, CTA 0), %6.2f ns/step (events)\n", grid,
+                   (double)*cyc / N_ITERS, ms * 1e6 / N_ITERS);
+        }
+    }
     for (auto& k : ks) {
         k.f<<<1, k.threads>>>(out, 1.0000001, cyc);
         cudaDeviceSynchronize();
