@@ -27,6 +27,11 @@ def main():
     p[:, 0, 2] = 1e5
     cases["airborne"] = (p, v)
     cases["seeds"] = (base_p, base_v)
+    p, v = base_p.copy(), base_v.copy()
+    p[0::2, 0, 2] = 0.0
+    v[0::2, 0, 2] = 0.0
+    p[1::2, 0, 2] = 1e5
+    cases["mixed"] = (p, v)
     out = {}
     for name, (p, v) in cases.items():
         if only and name != only:
