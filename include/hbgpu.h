@@ -104,6 +104,17 @@ hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 #define HB_KERNEL_GENERIC 1
 hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 
+/* Arithmetic of this context's stepping kernels.  HB_PRECISION_FP64
+ * (default) = the product path, bit-exact with simulate() (FP64 in the
+ * reference's operation order).  HB_PRECISION_FP32 = the FP32 throughput
+ * mode of SURVEY.md §8 row f3: float-float positions, FP32 increments,
+ * FMA-compensated constants; NOT bit-exact — fitness agrees with the FP64
+ * reference within a relative 1e-4 (tests/test_gpu_fp32.py), checksums are
+ * of this mode's own state.  Every model; host-built initial states. */
+#define HB_PRECISION_FP64 0
+#define HB_PRECISION_FP32 1
+hb_status hb_ctx_set_precision(hb_ctx* ctx, int precision);
+
 /* Zero-copy Box path (default on): when a Box batch's seeds and `out` are both
  * mapped page-locked memory (e.g. hb_host_alloc), the kernel reads the seeds
  * and writes the results through the host mapping — no H2D / D2H operation

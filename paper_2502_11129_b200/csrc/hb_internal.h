@@ -36,6 +36,9 @@ struct SimArgs {
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);
 const char* kernel_name(int kind, size_t n, int variant);
+// FP32 throughput mode (hb_fp32.cu; HB_PRECISION_FP32): host-built states only
+cudaError_t launch_sim_fp32(int kind, const SimArgs& a, cudaStream_t st);
+const char* kernel_name_fp32(int kind);
 cudaError_t launch_fp64_probe(double* scratch, int sms, int iters, cudaStream_t st, double* ops);
 cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, double* o0, double* o1,
                                   double* o2, double* o3, unsigned char* flags, cudaStream_t st);

@@ -264,6 +264,7 @@ struct hb_ctx {
     int device = 0;
     int sms = 148;
     int kernel_variant = HB_KERNEL_AUTO;
+    int precision = HB_PRECISION_FP64;
     cudaStream_t stream = nullptr;
     std::string err;
     ThreadPool* pool = nullptr;
@@ -282,6 +283,16 @@ struct hb_ctx {
     double* d_scratch = nullptr;
     double* d_ea_fit = nullptr;  // per-device fitness slice for the generation loop
     size_t d_ea_fit_cap = 0;
+    // generation-loop state on the selection device, kept across hb_run_ea
+    // calls (no per-call cudaMalloc / cudaFree / event creation)
+    uint64_t* d_ea_gen[2] = {nullptr, nullptr};
+    double* d_ea_pfit[2] = {nullptr, nullptr};
+    size_t d_ea_pop_cap = 0;
+    void* d_ea_scratch = nullptr;
+    size_t d_ea_scratch_cap = 0;
+    uint64_t* h_ea_gen = nullptr;  // pinned staging of the final population
+    double* h_ea_fit = nullptr;
+    cudaEvent_t ea_ev[3] = {nullptr, nullptr, nullptr};
 
     // pinned host buffers
     double* h_init = nullptr;
@@ -385,7 +396,7 @@ hb_status validate(hb_ctx* c, int kind, const void* seeds, size_t n, uint64_t st
 // Box in the optimised family builds its initial state on the device from
 // the seed; every other model gets the host initialiser (glibc cos / sin).
 bool init_on_device(const hb_ctx* c, int kind) {
-    return kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO;
+    return kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO && c->precision == HB_PRECISION_FP64;
 }
 
 constexpr size_t kParallelCopyMin = 2048;  // min items per host thread for copies / assembly
@@ -471,6 +482,12 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
     return HB_OK;
 }
 
+// One stepping launch of this context's kernel family / precision.
+cudaError_t launch_kernel(hb_ctx* c, int kind, const hb::SimArgs& a) {
+    if (c->precision == HB_PRECISION_FP32) return hb::launch_sim_fp32(kind, a, c->stream);
+    return hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant);
+}
+
 hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool from_seeds,
                  double* d_final) {
     if (c->counters_dirty) {
@@ -480,7 +497,7 @@ hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool 
     hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
                   c->d_out, c->d_fail, c->d_count, d_final, nullptr};
     c->last_steps = steps;
-    return c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch");
+    return c->cuda(launch_kernel(c, kind, a), "kernel launch");
 }
 
 // D2H of the compact records + failure count; assemble 32-byte
@@ -588,6 +605,10 @@ void hb_ctx_destroy(hb_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
     cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count); cudaFree(c->d_ea_fit);
+    for (int k = 0; k < 2; ++k) { cudaFree(c->d_ea_gen[k]); cudaFree(c->d_ea_pfit[k]); }
+    cudaFree(c->d_ea_scratch);
+    cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
+    for (cudaEvent_t e : c->ea_ev) if (e) cudaEventDestroy(e);
     cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
     cudaFreeHost(c->h_count);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -643,6 +664,14 @@ hb_status hb_ctx_set_zero_copy(hb_ctx* c, int enable) {
     return HB_OK;
 }
 
+hb_status hb_ctx_set_precision(hb_ctx* c, int precision) {
+    if (!c || (precision != HB_PRECISION_FP64 && precision != HB_PRECISION_FP32))
+        return set_global(HB_INVALID_ARG, "bad precision");
+    c->precision = precision;
+    c->staged_kind = -1;
+    return HB_OK;
+}
+
 hb_status hb_ctx_set_kernel(hb_ctx* c, int variant) {
     if (!c || (variant != HB_KERNEL_AUTO && variant != HB_KERNEL_GENERIC))
         return set_global(HB_INVALID_ARG, "bad kernel variant");
@@ -666,6 +695,7 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
                             uint64_t steps, hb_variant_result* out, uint64_t* fail_step, bool* any) {
     Trace tr("zero-copy");
     HB_TRY(ensure_capacity(c, hb::Box, n, false));
+    tr.mark("capacity");
     if (c->counters_dirty) {
         HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
         c->counters_dirty = false;
@@ -676,6 +706,7 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
     hb::SimArgs a{nullptr, dseeds, n, n, steps, hb::kSimDt, dout, c->d_fail, c->d_count, nullptr,
                   reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2)};
     c->staged_kind = -1;
+    tr.mark("args");
     HB_TRY(c->cuda(hb::launch_sim(hb::Box, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
     tr.mark("launch");
     HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
@@ -704,9 +735,12 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
                        hb_variant_result* out, uint64_t* fail_step, double* wall_time_s) {
     const auto t0 = std::chrono::steady_clock::now();
     HB_TRY(validate(c, kind, seeds, n, steps, out));
-    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO && c->zero_copy) {
+    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO && c->precision == HB_PRECISION_FP64 &&
+        c->zero_copy) {
+        Trace tr("ptrs");
         void* ds = mapped_device_ptr(seeds);
         void* dout = mapped_device_ptr(out);
+        tr.mark("lookup");
         if (ds && dout) {
             bool any = false;
             HB_TRY(run_box_zero_copy(c, static_cast<const uint64_t*>(ds),
@@ -1022,7 +1056,7 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
     }
     hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
                   c->d_out, c->d_fail, c->d_count, nullptr, nullptr};
-    HB_TRY(c->cuda(hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
+    HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
     HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                    c->stream), "D2H count"));
@@ -1057,6 +1091,12 @@ void enable_peer(int a, int b) {
 // on ctxs[0]'s stream after which src is valid.
 hb_status eval_sharded(hb_ctx* const* ctxs, int count, const std::vector<uint64_t>& shares, int kind,
                        const uint64_t* src, size_t n, uint64_t steps, double* dst, cudaEvent_t ready) {
+    if (count == 1) {  // one device: no helper thread
+        hb_ctx* c = ctxs[0];
+        HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+        HB_TRY(eval_start(c, kind, src, n, steps, dst));
+        return eval_finish(c, src, n, nullptr);
+    }
     std::vector<hb_status> st(count, HB_OK);
     std::vector<std::string> err(count);
     std::vector<std::thread> th;
@@ -1147,26 +1187,40 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     }
     HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
     const size_t mu = pop / 2;
-    uint64_t* d_gen[2] = {nullptr, nullptr};
-    double* d_fit[2] = {nullptr, nullptr};
-    void* scratch = nullptr;
     const size_t scratch_bytes = hb::ea_select_scratch_bytes(pop);
-    cudaEvent_t ev_ready, e0, e1, e2;
-    cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming);
-    cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
-    auto cleanup = [&] {
-        cudaSetDevice(c0->device);
-        for (int k = 0; k < 2; ++k) { cudaFree(d_gen[k]); cudaFree(d_fit[k]); }
-        cudaFree(scratch);
-        cudaEventDestroy(ev_ready); cudaEventDestroy(e0); cudaEventDestroy(e1); cudaEventDestroy(e2);
-    };
-    auto fail_out = [&](hb_status st) { cleanup(); return st; };
-    for (int k = 0; k < 2; ++k) {
-        if (c0->cuda(cudaMalloc(&d_gen[k], pop * sizeof(uint64_t)), "cudaMalloc") != HB_OK ||
-            c0->cuda(cudaMalloc(&d_fit[k], pop * sizeof(double)), "cudaMalloc") != HB_OK)
-            return fail_out(HB_CUDA_ERROR);
+    if (pop > c0->d_ea_pop_cap) {
+        for (int k = 0; k < 2; ++k) {
+            cudaFree(c0->d_ea_gen[k]); cudaFree(c0->d_ea_pfit[k]);
+            c0->d_ea_gen[k] = nullptr; c0->d_ea_pfit[k] = nullptr;
+        }
+        cudaFreeHost(c0->h_ea_gen); cudaFreeHost(c0->h_ea_fit);
+        c0->h_ea_gen = nullptr; c0->h_ea_fit = nullptr;
+        c0->d_ea_pop_cap = 0;
+        for (int k = 0; k < 2; ++k) {
+            HB_TRY(c0->cuda(cudaMalloc(&c0->d_ea_gen[k], pop * sizeof(uint64_t)), "cudaMalloc(ea genomes)"));
+            HB_TRY(c0->cuda(cudaMalloc(&c0->d_ea_pfit[k], pop * sizeof(double)), "cudaMalloc(ea fitness)"));
+        }
+        HB_TRY(c0->cuda(cudaHostAlloc(&c0->h_ea_gen, pop * sizeof(uint64_t), 0), "cudaHostAlloc(ea)"));
+        HB_TRY(c0->cuda(cudaHostAlloc(&c0->h_ea_fit, pop * sizeof(double), 0), "cudaHostAlloc(ea)"));
+        c0->d_ea_pop_cap = pop;
     }
-    if (c0->cuda(cudaMalloc(&scratch, scratch_bytes), "cudaMalloc") != HB_OK) return fail_out(HB_CUDA_ERROR);
+    if (scratch_bytes > c0->d_ea_scratch_cap) {
+        cudaFree(c0->d_ea_scratch);
+        c0->d_ea_scratch = nullptr;
+        c0->d_ea_scratch_cap = 0;
+        HB_TRY(c0->cuda(cudaMalloc(&c0->d_ea_scratch, scratch_bytes), "cudaMalloc(ea scratch)"));
+        c0->d_ea_scratch_cap = scratch_bytes;
+    }
+    if (!c0->ea_ev[0]) {
+        HB_TRY(c0->cuda(cudaEventCreateWithFlags(&c0->ea_ev[0], cudaEventDisableTiming), "event"));
+        HB_TRY(c0->cuda(cudaEventCreate(&c0->ea_ev[1]), "event"));
+        HB_TRY(c0->cuda(cudaEventCreate(&c0->ea_ev[2]), "event"));
+    }
+    uint64_t* d_gen[2] = {c0->d_ea_gen[0], c0->d_ea_gen[1]};
+    double* d_fit[2] = {c0->d_ea_pfit[0], c0->d_ea_pfit[1]};
+    void* scratch = c0->d_ea_scratch;
+    cudaEvent_t ev_ready = c0->ea_ev[0], e0 = c0->ea_ev[1], e2 = c0->ea_ev[2];
+    auto fail_out = [&](hb_status st) { return st; };
 
     std::vector<double> times(count, 1.0);
     if (device_times) for (int d = 0; d < count; ++d) times[d] = device_times[d];
@@ -1207,37 +1261,44 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
         HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
         cudaEventRecord(e0, c0->stream);
         cudaError_t e = hb::ea_select_vary(d_gen[cur], d_fit[cur], pop, g, d_gen[nxt], d_fit[nxt], scratch,
-                                           scratch_bytes, c0->stream);
+                                           c0->d_ea_scratch_cap, c0->stream);
         cudaEventRecord(e2, c0->stream);
         cudaEventRecord(ev_ready, c0->stream);
         if (c0->cuda(e, "select/vary") != HB_OK) return fail_out(HB_CUDA_ERROR);
-        if (c0->cuda(cudaEventSynchronize(e2), "sync") != HB_OK) return fail_out(HB_CUDA_ERROR);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, e0, e2);
-        sel_ms += ms;
-        prof.selection_s += elapsed_s(ts);
-        (void)e1;
         (void)var_ms;
-        // evaluate the offspring (ea.cpp:81-82)
+        // evaluate the offspring (ea.cpp:81-82); stream-ordered after the
+        // selection (device 0's stream, or a wait on ev_ready elsewhere) —
+        // the one host synchronisation per generation is the evaluation's
         te = clk::now();
         st = eval_sharded(ctxs, count, shares_for(mu), kind, d_gen[nxt] + mu, mu, steps, d_fit[nxt] + mu,
                           ev_ready);
-        prof.evaluation_s += elapsed_s(te);
         if (st != HB_OK) return fail_out(st);
+        // split the host interval by the selection's device time (e0 -> e2)
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e2);
+        sel_ms += ms;
+        const double span = elapsed_s(ts), sel = std::min(span, 1e-3 * ms);
+        prof.selection_s += sel;
+        prof.evaluation_s += span - sel;
+        (void)te;
         cur = nxt;
         if ((st = snapshot(cur, g)) != HB_OK) return fail_out(st);
     }
     // final population to the host
     tb = clk::now();
     HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
-    if (c0->cuda(cudaMemcpyAsync(genomes_out, d_gen[cur], pop * sizeof(uint64_t), cudaMemcpyDeviceToHost,
-                                 c0->stream), "D2H") != HB_OK ||
-        c0->cuda(cudaMemcpyAsync(fitness_out, d_fit[cur], pop * sizeof(double), cudaMemcpyDeviceToHost,
-                                 c0->stream), "D2H") != HB_OK ||
-        c0->cuda(cudaStreamSynchronize(c0->stream), "sync") != HB_OK)
-        return fail_out(HB_CUDA_ERROR);
+    {
+        const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
+        if (c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[cur], pop * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, c0->stream), "D2H") != HB_OK ||
+            c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[cur], pop * sizeof(double),
+                                     cudaMemcpyDeviceToHost, c0->stream), "D2H") != HB_OK ||
+            c0->cuda(cudaStreamSynchronize(c0->stream), "sync") != HB_OK)
+            return fail_out(HB_CUDA_ERROR);
+        if (!pg) std::memcpy(genomes_out, c0->h_ea_gen, pop * sizeof(uint64_t));
+        if (!pf) std::memcpy(fitness_out, c0->h_ea_fit, pop * sizeof(double));
+    }
     prof.bookkeeping_s += elapsed_s(tb);
-    cleanup();
     if (best_out) {
         double best = fitness_out[0];
         for (size_t i = 1; i < pop; ++i) best = std::max(best, fitness_out[i]);  // ea.cpp:101-103

@@ -200,6 +200,12 @@ class DeviceContext:
         """Box zero-copy path for pinned seeds + results (default on)."""
         self.check(lib.hb_ctx_set_zero_copy(self.handle, int(bool(enable))), "hb_ctx_set_zero_copy")
 
+    def set_precision(self, precision: int) -> None:
+        """_lib.HB_PRECISION_FP64 (bit-exact product path, default) or
+        _lib.HB_PRECISION_FP32 (throughput mode: float-float
+        positions, FP32 increments; fitness within 1e-4 relative, not bit-exact)."""
+        self.check(lib.hb_ctx_set_precision(self.handle, int(precision)), "hb_ctx_set_precision")
+
     def set_kernel(self, variant: int) -> None:
         """_lib.HB_KERNEL_AUTO (optimised) or _lib.HB_KERNEL_GENERIC (reference-order cross-check)."""
         self.check(lib.hb_ctx_set_kernel(self.handle, int(variant)), "hb_ctx_set_kernel")
@@ -225,11 +231,13 @@ class GpuExecutor(BatchExecutor):
     """The B200 accelerator back-end: one device, one persistent kernel per batch."""
 
     def __init__(self, device: int = 0, host_threads: int = 0, kernel: int = _lib.HB_KERNEL_AUTO,
-                 monitor: bool = False):
+                 monitor: bool = False, precision: int = _lib.HB_PRECISION_FP64):
         self.ctx = DeviceContext(device, host_threads)
         self.monitor = monitor  # NVML utilisation trace, like cpu_executor(monitor=true)
         if kernel != _lib.HB_KERNEL_AUTO:
             self.ctx.set_kernel(kernel)
+        if precision != _lib.HB_PRECISION_FP64:
+            self.ctx.set_precision(precision)
 
     def name(self) -> str:
         return "accel"

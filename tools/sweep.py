@@ -29,9 +29,10 @@ GRID = {
                      512000],
     "arm_with_rope": [32, 128, 256, 512, 1024, 2056, 4096, 8192, 16384, 32768, 65536, 131072, 256000],
     "humanoid": [32, 128, 256, 512, 1024, 2056, 4096, 8192, 16384, 32768],
+    "cpg_hinge": [32, 128, 256, 512, 1024, 2056, 4096, 8192, 16384, 32768, 65536, 131072],
 }
 STEPS = [100, 200, 500, 1000, 2000, 5000, 10000, 20000]
-W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240}
+W_ALG = {"box": 16, "box_and_ball": 200, "arm_with_rope": 2040, "humanoid": 8240, "cpg_hinge": 2204}
 
 
 def t_ci95(samples):
@@ -78,6 +79,16 @@ def knee(ns, walls):
 
 def cpu_rate(kind, steps=1000):
     import oracle as O
+    if int(kind) == 4:  # CpgHinge: no reference model; the oracle port, all host threads
+        cores = os.cpu_count() or 1
+        n = max(64 * cores, 4096)
+        steps = max(10, min(steps, int(3.0 * cores / (n * 1300e-9))))
+        seeds = np.arange(n, dtype=np.uint64)
+        t0 = time.perf_counter()
+        O.simulate_batch(4, seeds, steps, threads=cores)
+        wall = time.perf_counter() - t0
+        return {"value": n * steps / wall, "cores": cores, "kind": "port",
+                "sample": f"{n} variants x {steps} steps"}
     if not O.ref_available():
         return None
     cores = O.ref_hardware_concurrency()
@@ -96,7 +107,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="gpurun_out/sweeps.json")
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--models", default="box,box_and_ball,arm_with_rope,humanoid")
+    ap.add_argument("--models", default="box,box_and_ball,arm_with_rope,humanoid,cpg_hinge")
     a = ap.parse_args()
     ex = hb.GpuExecutor(0)
     peak, _ = ex.ctx.fp64_peak()
