@@ -327,6 +327,7 @@ def run_ours(a, ws, rank, local):
     barrier()
     torch.cuda.synchronize(dev)
     ctx.synchronize()
+    ops0 = ctx.work_counter() if a.model == "box" else 0
     t0 = time.perf_counter()
     with torch.cuda.stream(ext):
         for e0, e1 in evs:
@@ -344,6 +345,7 @@ def run_ours(a, ws, rank, local):
     ms_per_step = sum_ms / a.steps
     units = n_total * a.sim_steps  # variant-steps per bench step, all ranks
     value = units / (ms_per_step * 1e-3)
+    ops_exec = (ctx.work_counter() - ops0) / a.steps if a.model == "box" else None
     out, fail = ctx.fetch()
     assert int(np.sum(fail)) == 0, "blow-up in bench workload"
     _, replays = ctx.last_launch_stats()
@@ -361,6 +363,12 @@ def run_ours(a, ws, rank, local):
             "kernel": hb.kernel_name(kind, n),
             "kernel_ms_mean": float(np.mean(kernel_ms)),
             "exact_step_replays": replays,
+            # Box elides the z operations exactly at the grounded fixed point
+            # (DESIGN.md §3.1): the FP64 work the launch really executed, per
+            # the kernel's own counter, and the pipe fraction it implies
+            "executed_ops_per_launch": ops_exec,
+            "frac_executed": (None if ops_exec is None else
+                              ops_exec / (float(np.mean(kernel_ms)) * 1e-3) / peak_ops),
             "hbm_bytes_per_launch_algorithmic":
                 n * ((0 if a.model == "box" else
                       8 * (6 * BODIES[a.model] + CONS[a.model] + EXTRA_ROWS.get(a.model, 0)))

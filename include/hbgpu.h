@@ -138,6 +138,14 @@ hb_status hb_last_fail_steps(hb_ctx* ctx, uint64_t* fail_step, size_t n);
  * launches (the per-variant results are always the last launch's). */
 hb_status hb_last_launch_stats(hb_ctx* ctx, uint64_t* failed, uint64_t* exact_replays);
 
+/* Running total of the algorithmic FP64 operations this context's Box
+ * launches executed (16 per variant-step; 10 for the steps a
+ * warp ran at the exact grounded fixed point (p.z, v.z) = (+0, +0), whose z
+ * operations are elided; steps up to the failing one for a blown-up
+ * variant).  Read the difference around the launches of interest; it
+ * synchronises the context's stream.  Other models: W_alg x variant-steps. */
+hb_status hb_work_counter(hb_ctx* ctx, uint64_t* ops);
+
 /* ---- the drop-in call ------------------------------------------------------
  * batch_executor::run (executor.hpp:70) for `n` seeds through `steps` fixed
  * dt = kSimDt steps.  out[i] is the VariantResult of seeds[i] (seed order);

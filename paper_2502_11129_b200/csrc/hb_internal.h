@@ -32,6 +32,10 @@ struct SimArgs {
     // nullable: host-mapped flag a failing variant sets to 1 (plain store;
     // lets a zero-copy launch report "something blew up" without a D2H)
     volatile unsigned* fail_flag;
+    // nullable (Box): running total of the algorithmic FP64 ops the launch
+    // executed — 16 per variant-step, 10 for steps run at the grounded fixed
+    // point (z elided exactly); hb_work_counter reads it
+    unsigned long long* ops;
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);

@@ -302,6 +302,7 @@ struct hb_ctx {
     uint64_t* h_fail = nullptr;
     size_t h_n_cap = 0;
     unsigned* h_count = nullptr;
+    unsigned long long* d_ops = nullptr;  // Box executed-work counter (running total)
 
     // the batch currently resident on the device
     int staged_kind = -1;
@@ -495,7 +496,7 @@ hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool 
         c->counters_dirty = false;
     }
     hb::SimArgs a{from_seeds ? nullptr : c->d_init, c->d_seeds, n, n, steps, dt,
-                  c->d_out, c->d_fail, c->d_count, d_final, nullptr};
+                  c->d_out, c->d_fail, c->d_count, d_final, nullptr, c->d_ops};
     c->last_steps = steps;
     return c->cuda(launch_kernel(c, kind, a), "kernel launch");
 }
@@ -591,6 +592,8 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
         cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaMalloc(&c->d_scratch, 64) != cudaSuccess ||
         cudaMalloc(&c->d_count, 16) != cudaSuccess ||
+        cudaMalloc(&c->d_ops, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMemset(c->d_ops, 0, sizeof(unsigned long long)) != cudaSuccess ||
         cudaHostAlloc(&c->h_count, 16, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
         delete c;
         return set_global(HB_CUDA_ERROR, "stream/scratch creation failed");
@@ -605,6 +608,7 @@ void hb_ctx_destroy(hb_ctx* c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
     cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count); cudaFree(c->d_ea_fit);
+    cudaFree(c->d_ops);
     for (int k = 0; k < 2; ++k) { cudaFree(c->d_ea_gen[k]); cudaFree(c->d_ea_pfit[k]); }
     cudaFree(c->d_ea_scratch);
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
@@ -648,6 +652,16 @@ hb_status hb_last_fail_steps(hb_ctx* c, uint64_t* fail_step, size_t n) {
     if (n > c->last_n) return c->fail(HB_INVALID_ARG, "more failure steps requested than the batch had");
     if (c->last_failed) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
     else std::memset(fail_step, 0, n * sizeof(uint64_t));
+    return HB_OK;
+}
+
+hb_status hb_work_counter(hb_ctx* c, uint64_t* ops) {
+    if (!c || !ops) return set_global(HB_INVALID_ARG, "bad arguments");
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+    unsigned long long v = 0;
+    HB_TRY(c->cuda(cudaMemcpy(&v, c->d_ops, sizeof v, cudaMemcpyDeviceToHost), "D2H ops"));
+    *ops = v;
     return HB_OK;
 }
 
@@ -704,7 +718,7 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
     *flag = 0u;
     void* dflag = mapped_device_ptr(c->h_count);
     hb::SimArgs a{nullptr, dseeds, n, n, steps, hb::kSimDt, dout, c->d_fail, c->d_count, nullptr,
-                  reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2)};
+                  reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2), c->d_ops};
     c->staged_kind = -1;
     tr.mark("args");
     HB_TRY(c->cuda(hb::launch_sim(hb::Box, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
@@ -1055,7 +1069,7 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
         c->counters_dirty = false;
     }
     hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
-                  c->d_out, c->d_fail, c->d_count, nullptr, nullptr};
+                  c->d_out, c->d_fail, c->d_count, nullptr, nullptr, c->d_ops};
     HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
     HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
     HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,

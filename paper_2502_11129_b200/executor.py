@@ -200,6 +200,13 @@ class DeviceContext:
         """Box zero-copy path for pinned seeds + results (default on)."""
         self.check(lib.hb_ctx_set_zero_copy(self.handle, int(bool(enable))), "hb_ctx_set_zero_copy")
 
+    def work_counter(self) -> int:
+        """Running total of algorithmic FP64 ops executed by Box launches
+        (hb_work_counter; 16 per variant-step, 10 at the grounded fixed point)."""
+        v = C.c_uint64(0)
+        self.check(lib.hb_work_counter(self.handle, C.byref(v)), "hb_work_counter")
+        return int(v.value)
+
     def set_precision(self, precision: int) -> None:
         """_lib.HB_PRECISION_FP64 (bit-exact product path, default) or
         _lib.HB_PRECISION_FP32 (throughput mode: float-float

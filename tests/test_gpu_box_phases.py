@@ -122,3 +122,23 @@ def test_box_phases_partial_warp(gpu):
         got = gpu.run(hb.BatchRequest(0, seeds, 500)).results
         sub = slice(0, n, max(1, n // 150))
         assert np.array_equal(got[sub], O.simulate_batch(0, seeds[sub], 500).results)
+
+
+def test_box_work_counter(gpu):
+    """hb_work_counter: 16 algorithmic ops per variant-step, 10 for steps a
+    warp runs at the grounded fixed point; other models do not count."""
+    n, steps = 64, 1000
+    pos = np.zeros((n, 1, 3))
+    vel = np.zeros((n, 1, 3))
+    vel[:, 0, :2] = 0.25
+    c0 = gpu.ctx.work_counter()
+    gpu.run_states(0, pos, vel, np.zeros((n, 0)), steps=steps)
+    grounded = (steps // 16) * 16  # the horizon's whole chunks; the 8-step tail runs step()
+    assert gpu.ctx.work_counter() - c0 == n * (16 * steps - 6 * grounded)
+    c1 = gpu.ctx.work_counter()
+    gpu.run(hb.BatchRequest(1, np.arange(32, dtype=np.uint64), 100))
+    assert gpu.ctx.work_counter() == c1
+    seeds = np.arange(4096, dtype=np.uint64)
+    gpu.run(hb.BatchRequest(0, seeds, steps))
+    ops = gpu.ctx.work_counter() - c1
+    assert 10 * 4096 * steps < ops < 16 * 4096 * steps

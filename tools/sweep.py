@@ -127,12 +127,16 @@ def main():
                                    "knee": knee([r["n"] for r in rows], [r["wall_mean_s"] for r in rows])}
         srows = []
         for s in (STEPS[::2] if a.quick else STEPS):
+            ops0 = ex.ctx.work_counter()
             km = kernel_ms(ex, kind, 32768, s)
+            ops = (ex.ctx.work_counter() - ops0) / 4  # kernel_ms launches 1 warm-up + 3 timed
             walls = e2e_walls(ex, kind, 32768, s, 2)
             rate = 32768 * s / (km * 1e-3)
             srows.append({"steps": s, "kernel_ms": km, "rate_kernel": rate,
                           "rate_e2e": 32768 * s / float(np.min(walls)),
-                          "roofline_frac": W_ALG[m] * rate / peak})
+                          "roofline_frac": W_ALG[m] * rate / peak,
+                          "roofline_frac_executed": (ops / (km * 1e-3) / peak if m == "box" else
+                                                     W_ALG[m] * rate / peak)})
             print(m, "steps", s, "kernel %.3f ms" % km, flush=True)
         res["step_sweep"][m] = {"variants": 32768, "rows": srows}
     os.makedirs(os.path.dirname(os.path.abspath(a.out)), exist_ok=True)
