@@ -46,6 +46,22 @@ __global__ void select_vary_kernel(const uint64_t* genomes, const double* sorted
     next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
 }
 
+// The generation index from device memory (graph replays read the counter
+// the previous replay advanced).
+__global__ void select_vary_dev_g_kernel(const uint64_t* genomes, const double* sorted_fitness,
+                                         const uint32_t* order, size_t mu, const uint64_t* g_dev,
+                                         uint64_t* next, double* next_fit) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (i >= mu) return;
+    const uint64_t g = *g_dev;
+    const uint64_t parent = genomes[order[i]];
+    next[i] = parent;
+    next_fit[i] = sorted_fitness[i];
+    next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
+}
+
+__global__ void bump_kernel(uint64_t* g_dev) { *g_dev += 1; }
+
 __global__ void fitness_from_results_kernel(const hb_variant_result* out, size_t n, double* fitness) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i < n) fitness[i] = out[i].fitness;
@@ -79,9 +95,11 @@ size_t ea_select_scratch_bytes(size_t pop) {
     return al(temp) + al(pop * sizeof(double)) + 2 * al(pop * sizeof(uint32_t));
 }
 
-cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
-                           uint64_t* d_next, double* d_next_fit, void* scratch, size_t scratch_bytes,
-                           cudaStream_t st) {
+namespace {
+
+cudaError_t select_vary_impl(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
+                             uint64_t* g_dev, uint64_t* d_next, double* d_next_fit, void* scratch,
+                             size_t scratch_bytes, cudaStream_t st) {
     auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
     size_t temp = 0;
     cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, d_fitness, static_cast<double*>(nullptr),
@@ -100,9 +118,42 @@ cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, s
                                                               idx_out, static_cast<int>(pop), 0, 64, st);
     if (e != cudaSuccess) return e;
     const size_t mu = pop / 2;
-    select_vary_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, keys_out, idx_out, mu, g, d_next,
-                                                       d_next_fit);
+    if (g_dev) {
+        select_vary_dev_g_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, keys_out, idx_out, mu, g_dev,
+                                                                 d_next, d_next_fit);
+        bump_kernel<<<1, 1, 0, st>>>(g_dev);
+    } else {
+        select_vary_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, keys_out, idx_out, mu, g, d_next,
+                                                           d_next_fit);
+    }
     return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
+                           uint64_t* d_next, double* d_next_fit, void* scratch, size_t scratch_bytes,
+                           cudaStream_t st) {
+    return select_vary_impl(d_genomes, d_fitness, pop, g, nullptr, d_next, d_next_fit, scratch,
+                            scratch_bytes, st);
+}
+
+// The same selection + variation captured once as a CUDA graph (iota, the
+// radix sort's ~30 passes/launches, gather + offspring, counter bump) —
+// replays pay one launch instead of one per kernel.  g comes from *g_dev,
+// advanced by every replay.
+cudaError_t ea_select_vary_graph(const uint64_t* d_genomes, const double* d_fitness, size_t pop,
+                                 uint64_t* g_dev, uint64_t* d_next, double* d_next_fit, void* scratch,
+                                 size_t scratch_bytes, cudaStream_t st, cudaGraphExec_t* exec) {
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    e = select_vary_impl(d_genomes, d_fitness, pop, 0, g_dev, d_next, d_next_fit, scratch, scratch_bytes, st);
+    cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    return e;
 }
 
 }  // namespace hb

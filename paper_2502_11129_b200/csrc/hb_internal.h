@@ -55,5 +55,8 @@ size_t ea_select_scratch_bytes(size_t pop);
 cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, size_t pop, uint64_t g,
                            uint64_t* d_next, double* d_next_fit, void* scratch, size_t scratch_bytes,
                            cudaStream_t st);
+cudaError_t ea_select_vary_graph(const uint64_t* d_genomes, const double* d_fitness, size_t pop,
+                                 uint64_t* g_dev, uint64_t* d_next, double* d_next_fit, void* scratch,
+                                 size_t scratch_bytes, cudaStream_t st, cudaGraphExec_t* exec);
 
 }  // namespace hb

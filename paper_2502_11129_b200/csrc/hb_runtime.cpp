@@ -293,6 +293,9 @@ struct hb_ctx {
     uint64_t* h_ea_gen = nullptr;  // pinned staging of the final population
     double* h_ea_fit = nullptr;
     cudaEvent_t ea_ev[3] = {nullptr, nullptr, nullptr};
+    cudaGraphExec_t ea_graph[2] = {nullptr, nullptr};  // select/vary cur -> cur ^ 1, for d_ea_pop_cap
+    size_t ea_graph_pop = 0;
+    uint64_t* d_ea_g = nullptr;  // generation counter the graphs read and advance
 
     // pinned host buffers
     double* h_init = nullptr;
@@ -613,6 +616,8 @@ void hb_ctx_destroy(hb_ctx* c) {
     cudaFree(c->d_ea_scratch);
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
     for (cudaEvent_t e : c->ea_ev) if (e) cudaEventDestroy(e);
+    for (cudaGraphExec_t g : c->ea_graph) if (g) cudaGraphExecDestroy(g);
+    cudaFree(c->d_ea_g);
     cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
     cudaFreeHost(c->h_count);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -1218,6 +1223,13 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
         HB_TRY(c0->cuda(cudaHostAlloc(&c0->h_ea_fit, pop * sizeof(double), 0), "cudaHostAlloc(ea)"));
         c0->d_ea_pop_cap = pop;
     }
+    if (c0->ea_graph_pop != pop || scratch_bytes > c0->d_ea_scratch_cap) {
+        for (cudaGraphExec_t& g : c0->ea_graph) {
+            if (g) cudaGraphExecDestroy(g);
+            g = nullptr;
+        }
+        c0->ea_graph_pop = 0;
+    }
     if (scratch_bytes > c0->d_ea_scratch_cap) {
         cudaFree(c0->d_ea_scratch);
         c0->d_ea_scratch = nullptr;
@@ -1233,6 +1245,20 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     uint64_t* d_gen[2] = {c0->d_ea_gen[0], c0->d_ea_gen[1]};
     double* d_fit[2] = {c0->d_ea_pfit[0], c0->d_ea_pfit[1]};
     void* scratch = c0->d_ea_scratch;
+    if (!c0->d_ea_g) HB_TRY(c0->cuda(cudaMalloc(&c0->d_ea_g, sizeof(uint64_t)), "cudaMalloc(ea g)"));
+    if (c0->ea_graph_pop != pop) {
+        for (int k = 0; k < 2; ++k)
+            HB_TRY(c0->cuda(hb::ea_select_vary_graph(d_gen[k], d_fit[k], pop, c0->d_ea_g, d_gen[k ^ 1],
+                                                     d_fit[k ^ 1], scratch, c0->d_ea_scratch_cap,
+                                                     c0->stream, &c0->ea_graph[k]),
+                            "capture select/vary"));
+        c0->ea_graph_pop = pop;
+    }
+    {
+        static const uint64_t kFirstGeneration = 1;
+        HB_TRY(c0->cuda(cudaMemcpyAsync(c0->d_ea_g, &kFirstGeneration, sizeof(uint64_t),
+                                        cudaMemcpyHostToDevice, c0->stream), "H2D g"));
+    }
     cudaEvent_t ev_ready = c0->ea_ev[0], e0 = c0->ea_ev[1], e2 = c0->ea_ev[2];
     auto fail_out = [&](hb_status st) { return st; };
 
@@ -1274,8 +1300,7 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
         auto ts = clk::now();
         HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
         cudaEventRecord(e0, c0->stream);
-        cudaError_t e = hb::ea_select_vary(d_gen[cur], d_fit[cur], pop, g, d_gen[nxt], d_fit[nxt], scratch,
-                                           c0->d_ea_scratch_cap, c0->stream);
+        cudaError_t e = cudaGraphLaunch(c0->ea_graph[cur], c0->stream);  // generation g (device counter)
         cudaEventRecord(e2, c0->stream);
         cudaEventRecord(ev_ready, c0->stream);
         if (c0->cuda(e, "select/vary") != HB_OK) return fail_out(HB_CUDA_ERROR);
