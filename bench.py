@@ -472,8 +472,7 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
     def one():
         if ws == 1:
             return hb.run_ea(kind, pop, G, a.sim_steps, ex, seed=0)
-        return hbd.run_ea_sharded(kind, pop, G, a.sim_steps, ex, dist, seed=0,
-                                  device=red_dev if red_dev.type == "cuda" else None)
+        return hbd.run_ea_sharded_device(kind, pop, G, a.sim_steps, ex, dist, seed=0)
 
     def max_over_ranks(x):
         if dist is None:
@@ -515,7 +514,9 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
                         "d2h_bytes_per_step": 16 * pop,
                         "path": "run_ea -> hb_run_ea (genomes created and selected on the device; "
                                 "final population D2H)" if ws == 1 else
-                                "run_ea_sharded (host selection; NCCL fitness all-gather)"},
+                                "run_ea_sharded_device (device-resident population on every rank; "
+                                "offspring slices evaluated per rank, NCCL fitness all-gather, "
+                                "identical device selection on every rank; final population D2H)"},
                 "evaluation_fraction": ev / tot if tot else None,
                 "best_fitness": r.best_fitness, "clocks": clk,
                 "gpu_launches": a.steps * (G + 1) * (1 if ws == 1 else 1),

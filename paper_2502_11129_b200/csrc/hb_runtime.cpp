@@ -1178,12 +1178,22 @@ hb_status hb_ea_select_vary(hb_ctx* c, const uint64_t* d_genomes, const double* 
     if (pop < 2 || pop % 2) return c->fail(HB_INVALID_ARG, "run_ea: population_size must be even and >= 2");
     HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
     const size_t bytes = hb::ea_select_scratch_bytes(pop);
-    void* scratch = nullptr;
-    HB_TRY(c->cuda(cudaMallocAsync(&scratch, bytes, c->stream), "cudaMallocAsync"));
-    cudaError_t e = hb::ea_select_vary(d_genomes, d_fitness, pop, g, d_next, d_next_fitness, scratch, bytes,
-                                       c->stream);
-    cudaFreeAsync(scratch, c->stream);
-    return c->cuda(e, "select/vary");
+    if (bytes > c->d_ea_scratch_cap) {  // the context's persistent selection scratch
+        HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+        cudaFree(c->d_ea_scratch);
+        c->d_ea_scratch = nullptr;
+        c->d_ea_scratch_cap = 0;
+        for (cudaGraphExec_t& ge : c->ea_graph) {  // captured against the old scratch
+            if (ge) cudaGraphExecDestroy(ge);
+            ge = nullptr;
+        }
+        c->ea_graph_pop = 0;
+        HB_TRY(c->cuda(cudaMalloc(&c->d_ea_scratch, bytes), "cudaMalloc(ea scratch)"));
+        c->d_ea_scratch_cap = bytes;
+    }
+    return c->cuda(hb::ea_select_vary(d_genomes, d_fitness, pop, g, d_next, d_next_fitness, c->d_ea_scratch,
+                                      c->d_ea_scratch_cap, c->stream),
+                   "select/vary");
 }
 
 hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, int kind, size_t pop,

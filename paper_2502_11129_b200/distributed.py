@@ -87,3 +87,100 @@ def run_ea_sharded(kind: ModelKind, population_size: int, generations: int, step
     acc = prof.selection_s + prof.variation_s + prof.evaluation_s
     prof.bookkeeping_s = max(prof.total_s - acc, 0.0)
     return EaResult(pop, prof, float(np.max(pop.fitnesses)))
+
+
+def run_ea_sharded_device(kind: ModelKind, population_size: int, generations: int, steps: int,
+                          executor, dist, seed: int = 0, times=None) -> EaResult:
+    """The generation loop device-resident on every rank (one process per GPU).
+
+    Genomes and fitness live in each rank's HBM.  Per generation: this rank
+    evaluates its contiguous slice of the offspring from device memory
+    (hb_eval_device: device-side Box init / host initialiser, one stepping
+    launch); the fitness slices — plus each slice's blow-up count — are
+    all-gathered (NCCL over NVLink: 8 B / variant); every rank then runs the
+    identical device selection + variation (hb_ea_select_vary: stable radix
+    sort, parent gather, offspring hashing), so the populations stay equal
+    without any further exchange and nothing crosses to the host until the
+    end.  A blow-up anywhere aborts the loop on every rank, as batch_failure
+    aborts run_ea (ea.cpp:25).  Bit-identical to run_ea for any world size.
+    With a gloo group (tests: several ranks on one GPU) the all-gather goes
+    through host tensors.  hb_* calls run on the context's stream and torch
+    work on torch's current stream; the two are joined by host syncs at the
+    hand-overs (three per generation, a few µs each)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from ._lib import lib
+
+    if population_size < 2 or population_size % 2 != 0:
+        raise ValueError("run_ea: population_size must be even and >= 2")
+    if generations < 1:
+        raise ValueError("run_ea: generations must be >= 1")
+    ctx = executor.ctx
+    dev = torch.device("cuda", ctx.device)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    host_coll = dist.get_backend() == "gloo"
+    clock = time.perf_counter
+    prof = PhaseProfile()
+    t_start = clock()
+    pop_n, mu = population_size, population_size // 2
+
+    def evaluate(src, dst, n):
+        b = shard_bounds(n, world, times)
+        lo, hi = int(b[rank]), int(b[rank + 1])
+        width = int(np.max(np.diff(b)))
+        part = bufs[width]  # [fitness..., failures], reused across generations
+        failed = C.c_uint64(0)
+        if hi > lo:
+            # the context's stream; returns after synchronising it (blow-up count read)
+            st = lib.hb_eval_device(ctx.handle, int(kind), src.data_ptr() + 8 * lo, hi - lo, int(steps),
+                                    part.data_ptr(), C.byref(failed))
+            if st not in (_lib.HB_OK, _lib.HB_BLOWUP_PARTIAL):
+                raise RuntimeError(f"hb_eval_device failed [{st}]: {ctx.error()}")
+        part[width] = float(failed.value)
+        if host_coll:
+            src_part = part.cpu()
+            parts = [torch.empty_like(src_part) for _ in range(world)]
+            dist.all_gather(parts, src_part)
+        else:
+            flat = flats[width]
+            dist.all_gather_into_tensor(flat, part)
+            parts = list(flat.view(world, width + 1))
+        n_failed = int(torch.stack([p[width] for p in parts]).sum().item())  # one D2H per generation
+        if n_failed:
+            raise RuntimeError(f"run_ea: numerical blow-up during evaluation ({n_failed} variants)")
+        dst[:n].copy_(torch.cat([parts[r][: int(b[r + 1] - b[r])] for r in range(world)]).to(dev))
+        # hb_* calls run on the context's stream: finish torch's work first
+        torch.cuda.current_stream(dev).synchronize()
+
+    widths = {int(np.max(np.diff(shard_bounds(n, world, times)))) for n in (pop_n, mu)}
+    bufs = {w: torch.zeros(w + 1, dtype=torch.float64, device=dev) for w in widths}
+    flats = {w: torch.empty(world * (w + 1), dtype=torch.float64, device=dev) for w in widths}
+    gen = [torch.empty(pop_n, dtype=torch.int64, device=dev) for _ in range(2)]
+    fit = [torch.empty(pop_n, dtype=torch.float64, device=dev) for _ in range(2)]
+    torch.cuda.current_stream(dev).synchronize()  # buffers allocated before the context uses them
+    ctx.check(lib.hb_ea_init_genomes(ctx.handle, int(seed), pop_n, gen[0].data_ptr()), "init genomes")
+    t0 = clock()
+    evaluate(gen[0], fit[0], pop_n)
+    prof.evaluation_s += clock() - t0
+    cur = 0
+    for g in range(1, generations + 1):
+        nxt = cur ^ 1
+        t0 = clock()
+        ctx.check(lib.hb_ea_select_vary(ctx.handle, gen[cur].data_ptr(), fit[cur].data_ptr(), pop_n, g,
+                                        gen[nxt].data_ptr(), fit[nxt].data_ptr()), "select/vary")
+        prof.selection_s += clock() - t0
+        t0 = clock()
+        evaluate(gen[nxt][mu:], fit[nxt][mu:], mu)
+        prof.evaluation_s += clock() - t0
+        cur = nxt
+    ctx.synchronize()
+    genomes = gen[cur].cpu().numpy().view(np.uint64).copy()
+    fitness = fit[cur].cpu().numpy().copy()
+    prof.total_s = clock() - t_start
+    acc = prof.selection_s + prof.variation_s + prof.evaluation_s
+    prof.bookkeeping_s = max(prof.total_s - acc, 0.0)
+    pop = Population(genomes, fitness, generations)
+    return EaResult(pop, prof, float(np.max(fitness)))

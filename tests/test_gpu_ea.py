@@ -66,3 +66,52 @@ def test_native_preconditions(gpu):
     for pop, gens in ((5, 1), (0, 1), (4, 0)):
         with pytest.raises(ValueError):
             hb.run_ea(0, pop, gens, 10, gpu)
+
+
+def _sharded_worker(rank, world, port, kind, pop, gens, steps, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    import paper_2502_11129_b200 as hb2
+    from paper_2502_11129_b200 import distributed as hbd
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ex = hb2.GpuExecutor(0)
+        r = hbd.run_ea_sharded_device(kind, pop, gens, steps, ex, dist, seed=11)
+        q.put((rank, r.population.genomes.tolist(), r.population.fitnesses.tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_device_sharded_ea_equals_reference_loop(world):
+    """run_ea_sharded_device (the multi-GPU generation loop: device-resident
+    population, per-rank offspring slices, fitness all-gather, identical
+    device selection on every rank) — here `world` ranks share cuda:0 over
+    gloo — is bit-identical to run_ea over the oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    kind, pop, gens, steps = 1, 2048, 3, 120
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, kind, pop, gens, steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    ref = hb.run_ea(kind, pop, gens, steps, OracleExecutor(8), seed=11)
+    for _, g, f in out:
+        assert g == ref.population.genomes.tolist()
+        assert np.array_equal(np.array(f), ref.population.fitnesses)
