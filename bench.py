@@ -268,6 +268,20 @@ def run_reference(a, ws, rank):
     print(json.dumps(base))
 
 
+def latency_bound(a, n, ops_exec, kernel_ms, clk):
+    """Dependent-chain latency roofline of the Box kernel."""
+    if a.model != "box" or ops_exec is None:
+        return None
+    steps = a.sim_steps
+    gnd = max(0.0, (16.0 * n * steps - ops_exec) / (6.0 * n))  # average grounded steps per variant
+    cycles = 8.07 * (5.0 * gnd + 6.0 * (steps - gnd))
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    t_ideal_ms = cycles / (mhz * 1e6) * 1e3
+    return {"chain_cycles_per_variant": cycles, "grounded_steps_per_variant": gnd,
+            "ideal_ms": t_ideal_ms, "frac": t_ideal_ms / kernel_ms,
+            "model": "5 (grounded) or 6 (otherwise) dependent FP64 ops per step x 8.07 cycles"}
+
+
 # ---------------------------------------------------------------------- ours
 def run_ours(a, ws, rank, local):
     import torch
@@ -369,6 +383,12 @@ def run_ours(a, ws, rank, local):
             "executed_ops_per_launch": ops_exec,
             "frac_executed": (None if ops_exec is None else
                               ops_exec / (float(np.mean(kernel_ms)) * 1e-3) / peak_ops),
+            # The bound that actually binds Box at this size: one warp per
+            # SMSP, each step a dependent FP64 chain (5 ops grounded, 6 in
+            # flight / landing) at the measured 8.07-cycle DADD/DMUL latency
+            # (tools/ubench_fp64.cu).  Ideal time = that chain for the average
+            # variant's mix of grounded / other steps, at the sampled SM clock.
+            "latency_bound": latency_bound(a, n, ops_exec, float(np.mean(kernel_ms)), clk),
             "hbm_bytes_per_launch_algorithmic":
                 n * ((0 if a.model == "box" else
                       8 * (6 * BODIES[a.model] + CONS[a.model] + EXTRA_ROWS.get(a.model, 0)))
