@@ -306,7 +306,8 @@ def test_nvml_utilisation_trace():
     """GpuExecutor(monitor=True) fills BatchResult.utilization_trace from NVML
     (the accelerator side the reference leaves at 0, monitor.cpp:164)."""
     ex = hb.GpuExecutor(0, monitor=True)
-    res = ex.run(hb.BatchRequest(3, np.arange(16384, dtype=np.uint64), 3000))
+    # ~0.6 s of kernel time: several 20 Hz samples inside NVML's averaging window
+    res = ex.run(hb.BatchRequest(3, np.arange(16384, dtype=np.uint64), 15000))
     tr = res.utilization_trace
     assert len(tr) >= 2
     assert all(0.0 <= u <= 100.0 for _, u in tr)
