@@ -711,7 +711,7 @@ hb_status hb_build_states(int kind, const uint64_t* seeds, size_t n, double* soa
 // (zero-copy) — no H2D / D2H operations on the call's critical path; a
 // host-mapped flag tells whether anything blew up.
 static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant_result* dout, size_t n,
-                            uint64_t steps, hb_variant_result* out, uint64_t* fail_step, bool* any) {
+                                   uint64_t steps, uint64_t* fail_step, bool* any) {
     Trace tr("zero-copy");
     HB_TRY(ensure_capacity(c, hb::Box, n, false));
     tr.mark("capacity");
@@ -746,7 +746,6 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
         if (*any) std::memcpy(fail_step, c->h_fail, n * sizeof(uint64_t));
         else std::memset(fail_step, 0, n * sizeof(uint64_t));
     }
-    (void)out;
     return HB_OK;
 }
 
@@ -763,8 +762,7 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
         if (ds && dout) {
             bool any = false;
             HB_TRY(run_box_zero_copy(c, static_cast<const uint64_t*>(ds),
-                                     static_cast<hb_variant_result*>(dout), n, steps, out, fail_step,
-                                     &any));
+                                     static_cast<hb_variant_result*>(dout), n, steps, fail_step, &any));
             if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
             if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
             return HB_OK;
@@ -1270,7 +1268,6 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
                                         cudaMemcpyHostToDevice, c0->stream), "H2D g"));
     }
     cudaEvent_t ev_ready = c0->ea_ev[0], e0 = c0->ea_ev[1], e2 = c0->ea_ev[2];
-    auto fail_out = [&](hb_status st) { return st; };
 
     std::vector<double> times(count, 1.0);
     if (device_times) for (int d = 0; d < count; ++d) times[d] = device_times[d];
@@ -1292,58 +1289,49 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
 
     // initial population + evaluation (ea.cpp:48-54)
     auto tb = clk::now();
-    if (c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream), "init genomes") != HB_OK)
-        return fail_out(HB_CUDA_ERROR);
+    HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream), "init genomes"));
     cudaEventRecord(ev_ready, c0->stream);
     prof.bookkeeping_s += elapsed_s(tb);
     auto te = clk::now();
-    hb_status st = eval_sharded(ctxs, count, shares_for(pop), kind, d_gen[0], pop, steps, d_fit[0], ev_ready);
+    HB_TRY(eval_sharded(ctxs, count, shares_for(pop), kind, d_gen[0], pop, steps, d_fit[0], ev_ready));
     prof.evaluation_s += elapsed_s(te);
-    if (st != HB_OK) return fail_out(st);
-    if ((st = snapshot(0, 0)) != HB_OK) return fail_out(st);
+    HB_TRY(snapshot(0, 0));
 
     int cur = 0;
-    double sel_ms = 0.0, var_ms = 0.0;
     for (uint64_t g = 1; g <= generations; ++g) {
         const int nxt = cur ^ 1;
         // selection + variation on device 0 (ea.cpp:60-79)
         auto ts = clk::now();
         HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
         cudaEventRecord(e0, c0->stream);
-        cudaError_t e = cudaGraphLaunch(c0->ea_graph[cur], c0->stream);  // generation g (device counter)
+        const cudaError_t e = cudaGraphLaunch(c0->ea_graph[cur], c0->stream);  // generation g (device counter)
         cudaEventRecord(e2, c0->stream);
         cudaEventRecord(ev_ready, c0->stream);
-        if (c0->cuda(e, "select/vary") != HB_OK) return fail_out(HB_CUDA_ERROR);
-        (void)var_ms;
+        HB_TRY(c0->cuda(e, "select/vary"));
         // evaluate the offspring (ea.cpp:81-82); stream-ordered after the
         // selection (device 0's stream, or a wait on ev_ready elsewhere) —
         // the one host synchronisation per generation is the evaluation's
-        te = clk::now();
-        st = eval_sharded(ctxs, count, shares_for(mu), kind, d_gen[nxt] + mu, mu, steps, d_fit[nxt] + mu,
-                          ev_ready);
-        if (st != HB_OK) return fail_out(st);
+        HB_TRY(eval_sharded(ctxs, count, shares_for(mu), kind, d_gen[nxt] + mu, mu, steps, d_fit[nxt] + mu,
+                            ev_ready));
         // split the host interval by the selection's device time (e0 -> e2)
         float ms = 0.f;
         cudaEventElapsedTime(&ms, e0, e2);
-        sel_ms += ms;
         const double span = elapsed_s(ts), sel = std::min(span, 1e-3 * ms);
         prof.selection_s += sel;
         prof.evaluation_s += span - sel;
-        (void)te;
         cur = nxt;
-        if ((st = snapshot(cur, g)) != HB_OK) return fail_out(st);
+        HB_TRY(snapshot(cur, g));
     }
     // final population to the host
     tb = clk::now();
     HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
     {
         const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
-        if (c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[cur], pop * sizeof(uint64_t),
-                                     cudaMemcpyDeviceToHost, c0->stream), "D2H") != HB_OK ||
-            c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[cur], pop * sizeof(double),
-                                     cudaMemcpyDeviceToHost, c0->stream), "D2H") != HB_OK ||
-            c0->cuda(cudaStreamSynchronize(c0->stream), "sync") != HB_OK)
-            return fail_out(HB_CUDA_ERROR);
+        HB_TRY(c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[cur], pop * sizeof(uint64_t),
+                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
+        HB_TRY(c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[cur], pop * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
+        HB_TRY(c0->cuda(cudaStreamSynchronize(c0->stream), "sync"));
         if (!pg) std::memcpy(genomes_out, c0->h_ea_gen, pop * sizeof(uint64_t));
         if (!pf) std::memcpy(fitness_out, c0->h_ea_fit, pop * sizeof(double));
     }
@@ -1355,9 +1343,8 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     }
     prof.total_s = elapsed_s(t_start);
     // the device time of selection+variation is reported as selection (one
-    // fused sort + gather + offspring launch); host time beyond the named
-    // phases is bookkeeping (ea.cpp:95-97)
-    (void)sel_ms;
+    // graph: sort + gather + offspring); host time beyond the named phases
+    // is bookkeeping (ea.cpp:95-97)
     const double accounted = prof.selection_s + prof.variation_s + prof.evaluation_s + prof.bookkeeping_s;
     if (prof.total_s > accounted) prof.bookkeeping_s += prof.total_s - accounted;
     if (profile) *profile = prof;
