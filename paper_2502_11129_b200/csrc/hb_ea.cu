@@ -6,12 +6,16 @@
 //   offspring[i] = rng::at(parents[i] ^ kChildKey, (g << 32) + i)   ea.cpp:75-79
 //   population   = parents ++ offspring                            ea.cpp:84-91
 //
-// Selection is a stable LSD radix sort of (fitness, index) pairs in
-// descending key order.  Fitness = sqrt(dx*dx + dy*dy) is +0 or a positive
-// finite double for every completed variant (a blown-up variant aborts the
-// generation, as batch_failure aborts run_ea), so the radix order of the
-// IEEE bit patterns is the numeric order and equal keys keep their input
-// order — exactly the permutation std::stable_sort with `>` produces.
+// Selection = the permutation std::stable_sort with `>` produces: fitness
+// descending, ties in index order.  Fitness = sqrt(dx*dx + dy*dy) is +0 or a
+// positive finite double for every completed variant (a blown-up variant
+// aborts the generation, as batch_failure aborts run_ea), so the order of
+// the IEEE bit patterns is the numeric order.  The sort runs on the high 32
+// bits only (a stable 4-pass radix sort of (hi32, index) — half the passes
+// of a 64-bit key), then every run of equal high words, already in index
+// order, is re-sorted by (low 32 bits descending, index ascending) —
+// insertion sort by the run's first thread; runs are a few elements (two
+// fitness values agree in their top 32 bits ~2^-20 relative apart).
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -28,27 +32,55 @@ __global__ void init_genomes_kernel(uint64_t key, size_t pop, uint64_t* genomes)
     if (i < pop) genomes[i] = rng_at(key, i);
 }
 
-__global__ void iota_kernel(size_t n, uint32_t* idx) {
+// (high word of fitness[i], i)
+__global__ void key_hi_kernel(const double* fitness, size_t n, uint32_t* key, uint32_t* idx) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i < n) idx[i] = static_cast<uint32_t>(i);
+    if (i >= n) return;
+    key[i] = static_cast<uint32_t>(__double2hiint(fitness[i]));
+    idx[i] = static_cast<uint32_t>(i);
+}
+
+// Within each run of equal high words (index order after the stable sort),
+// order by low word descending, index ascending: the run's first position
+// insertion-sorts it.
+__global__ void tie_fix_kernel(const double* fitness, const uint32_t* key, size_t n, uint32_t* order) {
+    const size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (p >= n) return;
+    if (p > 0 && key[p - 1] == key[p]) return;        // not a run start
+    if (p + 1 >= n || key[p + 1] != key[p]) return;    // run of one
+    size_t end = p + 1;
+    while (end < n && key[end] == key[p]) ++end;
+    for (size_t a = p + 1; a < end; ++a) {
+        const uint32_t ia = order[a];
+        const uint32_t la = static_cast<uint32_t>(__double2loint(fitness[ia]));
+        size_t b = a;
+        while (b > p) {
+            const uint32_t ib = order[b - 1];
+            const uint32_t lb = static_cast<uint32_t>(__double2loint(fitness[ib]));
+            if (lb > la || (lb == la && ib < ia)) break;  // ib precedes ia
+            order[b] = ib;
+            --b;
+        }
+        order[b] = ia;
+    }
 }
 
 // next[0, mu) = parents (genomes[order[i]]), next_fit[0, mu) = their fitness;
 // next[mu + i] = offspring of parent i.
-__global__ void select_vary_kernel(const uint64_t* genomes, const double* sorted_fitness,
+__global__ void select_vary_kernel(const uint64_t* genomes, const double* fitness,
                                    const uint32_t* order, size_t mu, uint64_t g,
                                    uint64_t* next, double* next_fit) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i >= mu) return;
     const uint64_t parent = genomes[order[i]];
     next[i] = parent;
-    next_fit[i] = sorted_fitness[i];
+    next_fit[i] = fitness[order[i]];
     next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
 }
 
 // The generation index from device memory (graph replays read the counter
 // the previous replay advanced).
-__global__ void select_vary_dev_g_kernel(const uint64_t* genomes, const double* sorted_fitness,
+__global__ void select_vary_dev_g_kernel(const uint64_t* genomes, const double* fitness,
                                          const uint32_t* order, size_t mu, const uint64_t* g_dev,
                                          uint64_t* next, double* next_fit) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -56,7 +88,7 @@ __global__ void select_vary_dev_g_kernel(const uint64_t* genomes, const double* 
     const uint64_t g = *g_dev;
     const uint64_t parent = genomes[order[i]];
     next[i] = parent;
-    next_fit[i] = sorted_fitness[i];
+    next_fit[i] = fitness[order[i]];
     next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
 }
 
@@ -86,13 +118,13 @@ cudaError_t ea_fitness_from_results(const hb_variant_result* out, size_t n, doub
 
 size_t ea_select_scratch_bytes(size_t pop) {
     size_t temp = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, static_cast<const double*>(nullptr),
-                                              static_cast<double*>(nullptr),
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, static_cast<const uint32_t*>(nullptr),
+                                              static_cast<uint32_t*>(nullptr),
                                               static_cast<const uint32_t*>(nullptr),
                                               static_cast<uint32_t*>(nullptr), static_cast<int>(pop));
-    // + sorted keys (pop doubles) + two index arrays (pop u32 each), 256 B aligned
+    // + keys in / out and indices in / out (pop u32 each), 256 B aligned
     auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
-    return al(temp) + al(pop * sizeof(double)) + 2 * al(pop * sizeof(uint32_t));
+    return al(temp) + 4 * al(pop * sizeof(uint32_t));
 }
 
 namespace {
@@ -102,28 +134,30 @@ cudaError_t select_vary_impl(const uint64_t* d_genomes, const double* d_fitness,
                              size_t scratch_bytes, cudaStream_t st) {
     auto al = [](size_t b) { return (b + 255) & ~static_cast<size_t>(255); };
     size_t temp = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, d_fitness, static_cast<double*>(nullptr),
+    cub::DeviceRadixSort::SortPairsDescending(nullptr, temp, static_cast<const uint32_t*>(nullptr),
+                                              static_cast<uint32_t*>(nullptr),
                                               static_cast<const uint32_t*>(nullptr),
                                               static_cast<uint32_t*>(nullptr), static_cast<int>(pop));
+    const size_t words = al(pop * sizeof(uint32_t));
+    if (al(temp) + 4 * words > scratch_bytes) return cudaErrorInvalidValue;
     char* base = static_cast<char*>(scratch);
     void* d_temp = base;
-    double* keys_out = reinterpret_cast<double*>(base + al(temp));
-    uint32_t* idx_in = reinterpret_cast<uint32_t*>(base + al(temp) + al(pop * sizeof(double)));
-    uint32_t* idx_out = reinterpret_cast<uint32_t*>(base + al(temp) + al(pop * sizeof(double)) +
-                                                    al(pop * sizeof(uint32_t)));
-    if (al(temp) + al(pop * sizeof(double)) + 2 * al(pop * sizeof(uint32_t)) > scratch_bytes)
-        return cudaErrorInvalidValue;
-    iota_kernel<<<blocks_for(pop), 256, 0, st>>>(pop, idx_in);
-    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(d_temp, temp, d_fitness, keys_out, idx_in,
-                                                              idx_out, static_cast<int>(pop), 0, 64, st);
+    uint32_t* key_in = reinterpret_cast<uint32_t*>(base + al(temp));
+    uint32_t* key_out = reinterpret_cast<uint32_t*>(base + al(temp) + words);
+    uint32_t* idx_in = reinterpret_cast<uint32_t*>(base + al(temp) + 2 * words);
+    uint32_t* idx_out = reinterpret_cast<uint32_t*>(base + al(temp) + 3 * words);
+    key_hi_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, pop, key_in, idx_in);
+    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(d_temp, temp, key_in, key_out, idx_in, idx_out,
+                                                              static_cast<int>(pop), 0, 32, st);
     if (e != cudaSuccess) return e;
+    tie_fix_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, key_out, pop, idx_out);
     const size_t mu = pop / 2;
     if (g_dev) {
-        select_vary_dev_g_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, keys_out, idx_out, mu, g_dev,
+        select_vary_dev_g_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, d_fitness, idx_out, mu, g_dev,
                                                                  d_next, d_next_fit);
         bump_kernel<<<1, 1, 0, st>>>(g_dev);
     } else {
-        select_vary_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, keys_out, idx_out, mu, g, d_next,
+        select_vary_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, d_fitness, idx_out, mu, g, d_next,
                                                            d_next_fit);
     }
     return cudaGetLastError();

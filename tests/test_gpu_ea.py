@@ -115,3 +115,45 @@ def test_device_sharded_ea_equals_reference_loop(world):
     for _, g, f in out:
         assert g == ref.population.genomes.tolist()
         assert np.array_equal(np.array(f), ref.population.fitnesses)
+
+
+def test_select_vary_ties_match_stable_sort(gpu):
+    """hb_ea_select_vary on crafted fitness: exact duplicates, +0, long runs of
+    equal high words with different low words — parents and their order must
+    be std::stable_sort with `>` (ea.cpp:60-72), offspring the reference hash."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2502_11129_b200 import _lib
+    rng = np.random.default_rng(5)
+    pop = 4096
+    base = rng.uniform(0.01, 1.4, pop)
+    bits = base.view(np.uint64).copy()
+    grp = rng.integers(0, 40, pop)                      # 40 shared high words ...
+    hi_words = (rng.uniform(0.01, 1.4, 40).view(np.uint64) >> np.uint64(32))
+    sel = rng.random(pop) < 0.5
+    bits[sel] = (hi_words[grp[sel]] << np.uint64(32)) | (bits[sel] & np.uint64(0xFFFFFFFF))
+    fit = bits.view(np.float64).copy()
+    fit[rng.choice(pop, 300, replace=False)] = fit[rng.choice(pop, 300)]  # exact duplicates
+    fit[:7] = 0.0                                                          # +0 fitness
+    fit[100:140] = fit[99]                                                 # a long exact tie run
+    genomes = rng.integers(0, 2**63, pop, dtype=np.uint64)
+    dev = torch.device("cuda", 0)
+    d_gen = torch.from_numpy(genomes.view(np.int64)).to(dev)
+    d_fit = torch.from_numpy(fit).to(dev)
+    d_next = torch.empty_like(d_gen)
+    d_nfit = torch.empty_like(d_fit)
+    torch.cuda.synchronize()
+    g = 3
+    st = _lib.lib.hb_ea_select_vary(gpu.ctx.handle, d_gen.data_ptr(), d_fit.data_ptr(), pop, g,
+                                    d_next.data_ptr(), d_nfit.data_ptr())
+    assert st == _lib.HB_OK
+    gpu.ctx.synchronize()
+    order = np.argsort(-fit, kind="stable")[: pop // 2]
+    nxt = d_next.cpu().numpy().view(np.uint64)
+    assert np.array_equal(nxt[: pop // 2], genomes[order])
+    assert np.array_equal(d_nfit.cpu().numpy()[: pop // 2].view(np.uint64), fit[order].view(np.uint64))
+    ctr = (np.uint64(g) << np.uint64(32)) + np.arange(pop // 2, dtype=np.uint64)
+    assert np.array_equal(nxt[pop // 2:], hb.rng_at(genomes[order] ^ np.uint64(0x243F6A8885A308D3), ctr))
+    _ = C
