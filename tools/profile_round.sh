@@ -6,6 +6,8 @@
 #   models_8192x5000.jsonl  every multi-body model at the configs[2] size
 #   launches_box.csv        ncu launch list of the default bench command
 #   prof_box.ncu-rep        ncu --set full capture of one box_kernel launch
+#   bench_ea_*.json         configs[4] generation loop (box, box_and_ball) + reference arms
+#   sweeps.json             variant / step sweeps (tools/sweep.py)
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/bench_box.json 2> gpurun_out/bench_box.err
 timeout 600 python bench.py --impl reference > gpurun_out/bench_box_ref.json 2> gpurun_out/bench_box_ref.err
@@ -20,4 +22,9 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:box_kernel -s 3 -c 1 \
   -o gpurun_out/prof_box -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/ncu_full.log 2>&1
+for m in box box_and_ball; do
+  timeout 600 python bench.py --workload ea --model $m > gpurun_out/bench_ea_$m.json 2> /dev/null
+  timeout 600 python bench.py --workload ea --model $m --impl reference > gpurun_out/bench_ea_${m}_ref.json 2> /dev/null
+done
+timeout 1800 python tools/sweep.py --out gpurun_out/sweeps.json > gpurun_out/sweep.log 2>&1
 ls -la gpurun_out
