@@ -303,14 +303,23 @@ def run_ours(a, ws, rank, local):
     if a.workload == "ea":
         return run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind)
 
-    # Global batch + N-way splitter (equal calibrated GPUs -> equal shares).
+    # Global batch (variants per GPU x N) split by the paper's splitter
+    # retargeted to N GPUs: every rank times the same probe on its own GPU
+    # (calibrate_ranks), the times are all-gathered, and plan_allocation_n
+    # gives each rank a contiguous share in proportion to its throughput.
     n_total = a.variants * ws
-    shares = hb.plan_allocation_n([1.0] * ws, n_total)
+    ex = hb.GpuExecutor(local)
+    calib = None
+    if ws > 1:
+        from paper_2502_11129_b200 import distributed as hbd
+        calib = hbd.calibrate_ranks(kind, a.sim_steps, a.variants, ex, dist)
+        shares = hb.plan_allocation_n(calib, n_total)
+    else:
+        shares = [n_total]
     begin = sum(shares[:rank])
     seeds = np.arange(begin, begin + shares[rank], dtype=np.uint64)
     n = len(seeds)
 
-    ex = hb.GpuExecutor(local)
     ctx = ex.ctx
     ext = torch.cuda.ExternalStream(ctx.stream, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -464,6 +473,8 @@ def run_ours(a, ws, rank, local):
                            "sim_steps": a.sim_steps,
                            "parallelism": f"dp{ws} (independent variants; contiguous slices "
                                           "from plan_allocation_n)",
+                           "splitter": ({"calibration_wall_s": calib, "shares": [int(x) for x in shares]}
+                                        if calib else None),
                            "l2": "flushed between timed launches (256 MiB write outside the "
                                  "event pair)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,

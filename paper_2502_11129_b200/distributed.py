@@ -28,6 +28,28 @@ def shard_bounds(n: int, world: int, times=None) -> np.ndarray:
     return np.concatenate([[0], np.cumsum(shares)]).astype(np.int64)
 
 
+def calibrate_ranks(kind: ModelKind, steps: int, probe_n: int, executor: BatchExecutor, dist,
+                    repeats: int = 3):
+    """The paper's calibration step (scheduler.cpp:30-56) across the ranks of
+    the default group: every rank times the same probe (seeds 0..probe_n-1,
+    best of `repeats` drop-in calls, wall_time_s) on its own device at once,
+    and the per-rank times are all-gathered, so every rank holds the same
+    times — the input of the N-way splitter (plan_allocation_n), which then
+    gives each rank a share in proportion to its measured throughput."""
+    import torch
+    if probe_n < 1:
+        raise ValueError("calibrate: probe_n must be >= 1")
+    req = BatchRequest(kind, np.arange(probe_n, dtype=np.uint64), steps)
+    best = min(executor.run(req).wall_time_s for _ in range(max(1, repeats)))
+    world = dist.get_world_size()
+    mine = torch.tensor([best], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        mine = mine.cuda()
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine)
+    return [float(t.item()) for t in parts]
+
+
 def evaluate_sharded(kind: ModelKind, genomes: np.ndarray, steps: int, executor: BatchExecutor,
                      dist, device=None, times=None) -> np.ndarray:
     """Fitness of every genome; this rank simulates only its slice."""

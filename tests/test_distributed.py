@@ -70,3 +70,35 @@ def test_shard_bounds_cover_contiguously():
             b = hbd.shard_bounds(n, world)
             assert b[0] == 0 and b[-1] == n and np.all(np.diff(b) >= 0)
             assert np.max(np.diff(b)) - np.min(np.diff(b)) <= world
+
+
+def _calib_worker(rank, world, port, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from helpers import OracleExecutor
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        times = hbd.calibrate_ranks(1, 30, 64, OracleExecutor(1), dist, repeats=2)
+        q.put((rank, times, [int(x) for x in hb.plan_allocation_n(times, 1000)]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_calibrate_ranks_world2_same_times_and_shares():
+    """Every rank times the probe on its own back-end; all ranks end with the
+    same time vector and hence the same splitter shares (sum = batch)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_calib_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, t0, s0), (_, t1, s1) = out
+    assert t0 == t1 and len(t0) == 2 and all(t > 0 for t in t0)
+    assert s0 == s1 and sum(s0) == 1000
