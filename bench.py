@@ -500,10 +500,15 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
     pop, G = a.population, a.generations
     evaluated = pop + G * (pop // 2)
 
+    # N > 1: the splitter's shares come from every rank timing the same probe
+    # (an offspring slice's worth of variants) on its own GPU
+    times = (hbd.calibrate_ranks(kind, a.sim_steps, max(1, (pop // 2) // ws), ex, dist)
+             if ws > 1 else None)
+
     def one():
         if ws == 1:
             return hb.run_ea(kind, pop, G, a.sim_steps, ex, seed=0)
-        return hbd.run_ea_sharded_device(kind, pop, G, a.sim_steps, ex, dist, seed=0)
+        return hbd.run_ea_sharded_device(kind, pop, G, a.sim_steps, ex, dist, seed=0, times=times)
 
     def max_over_ranks(x):
         if dist is None:
