@@ -39,6 +39,16 @@ struct SimArgs {
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);
+// The Box stepping launch through a per-context one-node CUDA graph whose
+// kernel parameters are updated in place each call: cheaper on the host and
+// on the device than a plain launch (the drop-in call's fixed cost).
+struct BoxGraph {
+    cudaGraph_t graph[2] = {nullptr, nullptr};  // [from seeds, from states]
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    cudaGraphNode_t node[2] = {nullptr, nullptr};
+};
+cudaError_t launch_box_graph(BoxGraph& g, const SimArgs& a, cudaStream_t st, int sms);
+void destroy_box_graph(BoxGraph& g);
 const char* kernel_name(int kind, size_t n, int variant);
 // FP32 throughput mode (hb_fp32.cu; HB_PRECISION_FP32): host-built states only
 cudaError_t launch_sim_fp32(int kind, const SimArgs& a, cudaStream_t st);

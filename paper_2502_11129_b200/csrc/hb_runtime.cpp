@@ -265,6 +265,7 @@ struct hb_ctx {
     int sms = 148;
     int kernel_variant = HB_KERNEL_AUTO;
     int precision = HB_PRECISION_FP64;
+    hb::BoxGraph box_graph;  // Box launches (optimised family, FP64)
     cudaStream_t stream = nullptr;
     std::string err;
     ThreadPool* pool = nullptr;
@@ -489,6 +490,8 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
 // One stepping launch of this context's kernel family / precision.
 cudaError_t launch_kernel(hb_ctx* c, int kind, const hb::SimArgs& a) {
     if (c->precision == HB_PRECISION_FP32) return hb::launch_sim_fp32(kind, a, c->stream);
+    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO)
+        return hb::launch_box_graph(c->box_graph, a, c->stream, c->sms);
     return hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant);
 }
 
@@ -612,6 +615,7 @@ void hb_ctx_destroy(hb_ctx* c) {
     cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
     cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count); cudaFree(c->d_ea_fit);
     cudaFree(c->d_ops);
+    hb::destroy_box_graph(c->box_graph);
     for (int k = 0; k < 2; ++k) { cudaFree(c->d_ea_gen[k]); cudaFree(c->d_ea_pfit[k]); }
     cudaFree(c->d_ea_scratch);
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
@@ -726,7 +730,7 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
                   reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2), c->d_ops};
     c->staged_kind = -1;
     tr.mark("args");
-    HB_TRY(c->cuda(hb::launch_sim(hb::Box, a, c->stream, c->sms, c->kernel_variant), "kernel launch"));
+    HB_TRY(c->cuda(launch_kernel(c, hb::Box, a), "kernel launch"));
     tr.mark("launch");
     HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
     tr.mark("sync");
