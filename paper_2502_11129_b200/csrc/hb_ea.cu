@@ -16,6 +16,8 @@
 // order, is re-sorted by (low 32 bits descending, index ascending) —
 // insertion sort by the run's first thread; runs are a few elements (two
 // fitness values agree in their top 32 bits ~2^-20 relative apart).
+#include <cooperative_groups.h>
+#include <cub/block/block_radix_rank.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -101,6 +103,150 @@ __global__ void fitness_from_results_kernel(const hb_variant_result* out, size_t
 
 unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
+// ---------------------------------------------------------------------------
+// One-cluster radix sort of up to 65 536 (high word, index) pairs: the
+// stable 4-pass LSD sort of the selection in a single launch.  8 CTAs of
+// 1 024 threads (a portable cluster) each hold an 8 192-item tile in shared
+// memory; per 8-bit digit pass every CTA ranks its tile stably
+// (cub::BlockRadixRankMatch), the CTAs exchange their digit histograms through
+// distributed shared memory, and every item is scattered straight into its
+// destination CTA's next tile (st.shared::cluster).  Sorting ~high word
+// ascending = high word descending; padding (index >= n) gets the largest
+// key and higher indices, so it ends up after every real item.  Replaces the
+// ~20 launches of the device-wide sort (the passes are latency-bound at
+// this size).
+constexpr int kSortCtas = 8, kSortThreads = 1024, kSortItems = 8;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 8 192
+constexpr int kSortMax = kSortCtas * kSortTile;       // 65 536
+using SortRank = cub::BlockRadixRankMatch<kSortThreads, 8, false>;  // match.any ranking: small per-warp counters
+
+struct SortSmem {
+    uint2 buf[kSortTile];  // (key, index): every CTA has read its tile into registers
+                           // before the histogram barrier, so the scatter after
+                           // it may overwrite the tile in place
+    typename SortRank::TempStorage rank;
+    int hist[256];    // this CTA's digit counts (read by the whole cluster)
+    int prefix[256];  // this CTA's exclusive digit prefix
+    int goff[256];    // global start of this CTA's items of each digit
+    int tot[256];
+};
+
+struct DigitAt {
+    uint32_t shift;
+    __device__ __forceinline__ uint32_t Digit(uint32_t k) const { return (k >> shift) & 0xffu; }
+};
+
+__global__ void __launch_bounds__(kSortThreads)
+cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out) {
+    namespace cg = cooperative_groups;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    cg::cluster_group cluster = cg::this_cluster();
+    const int c = static_cast<int>(cluster.block_rank());
+    const int t = threadIdx.x;
+    // warp-striped: item j of lane l in warp w is tile position w*32*K + 32j + l —
+    // the order BlockRadixRankMatch ranks ties in (warp, item, lane), so the
+    // ranking is stable with respect to tile order
+    const int stripe = (t >> 5) * 32 * kSortItems + (t & 31);
+    uint32_t key[kSortItems], idx[kSortItems];
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int e = c * kSortTile + stripe + 32 * j;
+        idx[j] = static_cast<uint32_t>(e);
+        key[j] = e < n ? ~static_cast<uint32_t>(__double2hiint(fitness[e])) : 0xffffffffu;
+    }
+    for (int pass = 0; pass < 4; ++pass) {
+        int ranks[kSortItems];
+        int excl[1];
+        SortRank(sm.rank).RankKeys(key, ranks, DigitAt{8u * pass}, excl);
+        if (t < 256) sm.prefix[t] = excl[0];
+        __syncthreads();
+        if (t < 256) sm.hist[t] = (t < 255 ? sm.prefix[t + 1] : kSortTile) - sm.prefix[t];
+        cluster.sync();  // every CTA's histogram is visible
+        if (t < 256) {
+            int tot = 0, before = 0;
+#pragma unroll
+            for (int r = 0; r < kSortCtas; ++r) {
+                const int v = cluster.map_shared_rank(sm.hist, r)[t];
+                tot += v;
+                before += r < c ? v : 0;
+            }
+            sm.tot[t] = tot;
+            sm.goff[t] = before;
+        }
+        __syncthreads();
+        if (t < 32) {  // exclusive scan of the 256 digit totals: one warp, 8 digits per lane
+            int v[8], sum = 0;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) { v[d] = sm.tot[8 * t + d]; sum += v[d]; }
+            int incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int u = __shfl_up_sync(0xffffffffu, incl, o);
+                if (t >= o) incl += u;
+            }
+            int run = incl - sum;
+#pragma unroll
+            for (int d = 0; d < 8; ++d) { sm.goff[8 * t + d] += run; run += v[d]; }
+        }
+        __syncthreads();
+        uint2* next = sm.buf;
+        const uint32_t next_sa = static_cast<uint32_t>(__cvta_generic_to_shared(next));
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const uint32_t d = (key[j] >> (8 * pass)) & 0xffu;
+            const int pos = sm.goff[d] + ranks[j] - sm.prefix[d];
+            // st.shared::cluster into the destination CTA's tile (mapa: the
+            // same shared-window offset in CTA pos / tile)
+            const uint32_t local = next_sa + static_cast<uint32_t>(pos % kSortTile) * 8u;
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(pos / kSortTile));
+            asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" :: "r"(remote), "r"(key[j]), "r"(idx[j])
+                         : "memory");
+        }
+        cluster.sync();  // every item has arrived in its tile
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const uint2 kv = next[stripe + 32 * j];
+            key[j] = kv.x;
+            idx[j] = kv.y;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kSortItems; ++j) {
+        const int p = c * kSortTile + stripe + 32 * j;
+        if (p < n) {
+            key_out[p] = ~key[j];
+            idx_out[p] = idx[j];
+        }
+    }
+    cluster.sync();  // no CTA leaves while another may still read its shared memory
+}
+
+cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
+                                cudaStream_t st) {
+    static bool attr_done = false;  // per process; the attribute is per function
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sizeof(SortSmem)));
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kSortCtas);
+    cfg.blockDim = dim3(kSortThreads);
+    cfg.dynamicSmemBytes = sizeof(SortSmem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kSortCtas;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, cluster_sort_kernel, fitness, n, key_out, idx_out);
+}
+
 }  // namespace
 
 cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st) {
@@ -146,9 +292,14 @@ cudaError_t select_vary_impl(const uint64_t* d_genomes, const double* d_fitness,
     uint32_t* key_out = reinterpret_cast<uint32_t*>(base + al(temp) + words);
     uint32_t* idx_in = reinterpret_cast<uint32_t*>(base + al(temp) + 2 * words);
     uint32_t* idx_out = reinterpret_cast<uint32_t*>(base + al(temp) + 3 * words);
-    key_hi_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, pop, key_in, idx_in);
-    cudaError_t e = cub::DeviceRadixSort::SortPairsDescending(d_temp, temp, key_in, key_out, idx_in, idx_out,
-                                                              static_cast<int>(pop), 0, 32, st);
+    cudaError_t e;
+    if (pop <= static_cast<size_t>(kSortMax)) {  // one cluster, one launch
+        e = launch_cluster_sort(d_fitness, static_cast<int>(pop), key_out, idx_out, st);
+    } else {
+        key_hi_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, pop, key_in, idx_in);
+        e = cub::DeviceRadixSort::SortPairsDescending(d_temp, temp, key_in, key_out, idx_in, idx_out,
+                                                      static_cast<int>(pop), 0, 32, st);
+    }
     if (e != cudaSuccess) return e;
     tie_fix_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, key_out, pop, idx_out);
     const size_t mu = pop / 2;
