@@ -117,17 +117,19 @@ def test_device_sharded_ea_equals_reference_loop(world):
         assert np.array_equal(np.array(f), ref.population.fitnesses)
 
 
-def test_select_vary_ties_match_stable_sort(gpu):
+@pytest.mark.parametrize("pop", [4096, 40002, 65536, 70000])
+def test_select_vary_ties_match_stable_sort(gpu, pop):
     """hb_ea_select_vary on crafted fitness: exact duplicates, +0, long runs of
     equal high words with different low words — parents and their order must
-    be std::stable_sort with `>` (ea.cpp:60-72), offspring the reference hash."""
+    be std::stable_sort with `>` (ea.cpp:60-72), offspring the reference hash.
+    Populations below / at the cluster sort's 65 536 (partial and full tiles)
+    and above it (the device-wide sort)."""
     import ctypes as C
 
     import torch
 
     from paper_2502_11129_b200 import _lib
-    rng = np.random.default_rng(5)
-    pop = 4096
+    rng = np.random.default_rng(5 + pop)
     base = rng.uniform(0.01, 1.4, pop)
     bits = base.view(np.uint64).copy()
     grp = rng.integers(0, 40, pop)                      # 40 shared high words ...
