@@ -107,10 +107,11 @@ hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
 /* Arithmetic of this context's stepping kernels.  HB_PRECISION_FP64
  * (default) = the product path, bit-exact with simulate() (FP64 in the
  * reference's operation order).  HB_PRECISION_FP32 = the FP32 throughput
- * mode of SURVEY.md §8 row f3: float-float positions, FP32 increments,
- * FMA-compensated constants; NOT bit-exact — fitness agrees with the FP64
- * reference within a relative 1e-4 (tests/test_gpu_fp32.py), checksums are
- * of this mode's own state.  Every model; host-built initial states. */
+ * mode of SURVEY.md §8 row f3 for the multi-body models: float-float
+ * positions, FP32 increments, FMA-compensated constants, MUFU rsqrt; NOT
+ * bit-exact — fitness within the tolerance stated in tests/test_gpu_fp32.py,
+ * checksums of this mode's own state; host-built initial states.  Box keeps
+ * the (faster) bit-exact FP64 kernel in either mode. */
 #define HB_PRECISION_FP64 0
 #define HB_PRECISION_FP32 1
 hb_status hb_ctx_set_precision(hb_ctx* ctx, int precision);

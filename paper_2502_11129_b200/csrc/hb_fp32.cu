@@ -1,4 +1,5 @@
-// hb_fp32.cu — FP32 throughput mode.  NOT bit-exact:
+// hb_fp32.cu — FP32 throughput mode for the
+// multi-body models (Box keeps the FP64 kernel in every mode).  NOT bit-exact:
 // the product path is the FP64 kernel family in hb_kernels.cu; this mode is
 // opt-in per context (hb_ctx_set_precision(ctx, HB_PRECISION_FP32)) and is
 // checked against the FP64 oracle within a stated relative tolerance
@@ -138,8 +139,14 @@ __global__ void __launch_bounds__(64) ff_kernel(SimArgs a) {
             const FF t = two_sum(p[r].hi, d.hi);
             q[r] = FF{t.hi, __fadd_rn(t.lo, __fadd_rn(p[r].lo, d.lo))};
         }
-        // 8 Gauss-Seidel sweeps in list order, ground clamp after each (:140-152)
-#pragma unroll 1
+        // 8 Gauss-Seidel sweeps in list order, ground clamp after each
+        // (:140-152).  Branch-free and fully unrolled (humanoid: one sweep per
+        // trip, registers), so ptxas sees the whole dependency DAG and
+        // overlaps independent links across sweeps (the wavefront) itself.
+        // dist and 1/dist come from one MUFU rsqrt (~2 ulp: inside this
+        // mode's tolerance); the degenerate link (dist < 1e-12, :144) is
+        // masked to a zero correction instead of skipped.
+#pragma unroll (K == Humanoid ? 1 : kIters)
         for (int it = 0; it < kIters; ++it) {
 #pragma unroll
             for (int c = 0; c < m; ++c) {
@@ -148,11 +155,11 @@ __global__ void __launch_bounds__(64) ff_kernel(SimArgs a) {
                 const float dy = diff_f(q[3 * B + 1], q[3 * A + 1]);
                 const float dz = diff_f(q[3 * B + 2], q[3 * A + 2]);
                 const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, __fmul_rn(dx, dx)));
-                const float dist = __fsqrt_rn(d2);
-                if (dist < 1e-12f) continue;
+                const float inv = rsqrtf(d2);
+                const float dist = __fmul_rn(d2, inv);
                 const float hk = con_soft(K, c) ? f.half_k_soft : f.half_k_stiff;
                 const float stretch = __fsub_rn(__fsub_rn(dist, rest[c].hi), rest[c].lo);
-                const float corr = __fdiv_rn(__fmul_rn(hk, stretch), dist);
+                const float corr = d2 > 1e-24f ? __fmul_rn(__fmul_rn(hk, stretch), inv) : 0.0f;
                 const float ex = __fmul_rn(dx, corr), ey = __fmul_rn(dy, corr), ez = __fmul_rn(dz, corr);
                 q[3 * A].lo = __fadd_rn(q[3 * A].lo, ex);
                 q[3 * A + 1].lo = __fadd_rn(q[3 * A + 1].lo, ey);
