@@ -142,19 +142,25 @@ def load_traffic(model, variants, sim_steps):
         return None
 
 
-def cpu_reference_rate(model_idx, n, sim_steps, reps=3):
-    """Reference cpu_executor(workers = hardware_concurrency) on the host; best
-    of `reps` runs of a bounded sample (the full workload when it is small)."""
+CPU_SAMPLE_S = 25.0  # CPU-work budget of the in-run baseline sample (estimate; ~10 s measured)
+
+
+def cpu_reference_rate(model_idx, n, sim_steps):
+    """Reference cpu_executor(workers = hardware_concurrency) on the host, on a
+    bounded sample of the workload (the full batch when one run is cheap,
+    else N' = max(64 x cores, 4096) variants), repeated for ~CPU_SAMPLE_S of
+    CPU work; reports the best run (the most favourable CPU figure) and the
+    median."""
     import oracle as O
     if model_idx == 4:
-        return cpu_port_rate(model_idx, n, sim_steps, reps)
+        return cpu_port_rate(model_idx, n, sim_steps)
     if not O.ref_available():
         return None
     cores = O.ref_hardware_concurrency()
-    per_vs_core_ns = PER_VS_CORE_NS[model_idx]
-    est_s = n * sim_steps * per_vs_core_ns * 1e-9 / cores * reps
-    # the full workload when it is cheap, else N' = max(64 x cores, 4096) variants
-    n_s = n if est_s <= 30.0 else min(n, max(64 * cores, 4096))
+    per_run_s = n * sim_steps * PER_VS_CORE_NS[model_idx] * 1e-9 / cores
+    n_s = n if per_run_s <= 10.0 else min(n, max(64 * cores, 4096))
+    per_run_s *= n_s / n
+    reps = int(min(400, max(3, CPU_SAMPLE_S / max(per_run_s, 1e-6))))
     seeds = np.arange(n_s, dtype=np.uint64)
     walls = []
     for _ in range(reps):
@@ -165,9 +171,11 @@ def cpu_reference_rate(model_idx, n, sim_steps, reps=3):
     best = min(walls)
     return {"value": n_s * sim_steps / best, "unit": "variant-steps/s", "cores": cores,
             "kind": "reference",
+            "median_value": n_s * sim_steps / float(np.median(walls)),
             "sample": f"{MODELS[model_idx]} {n_s} variants x {sim_steps} steps, seeds 0..{n_s - 1}, "
-                      f"reference cpu_executor(workers=0 -> {cores} threads), best of {reps}",
-            "walls_s": walls}
+                      f"reference cpu_executor(workers=0 -> {cores} threads), best of {reps} runs "
+                      f"({sum(walls):.1f} s)",
+            "walls_s_min_max": [best, max(walls)]}
 
 
 def cpu_port_rate(model_idx, n, sim_steps, reps=3):
@@ -176,7 +184,7 @@ def cpu_port_rate(model_idx, n, sim_steps, reps=3):
     import oracle as O
     cores = os.cpu_count() or 1
     est_s = n * sim_steps * PER_VS_CORE_NS[model_idx] * 1e-9 / cores * reps
-    n_s = n if est_s <= 30.0 else min(n, max(64 * cores, 4096))
+    n_s = n if est_s <= CPU_SAMPLE_S else min(n, max(64 * cores, 4096))
     seeds = np.arange(n_s, dtype=np.uint64)
     walls = []
     for _ in range(reps):
