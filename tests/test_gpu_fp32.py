@@ -87,3 +87,29 @@ def test_fp32_selection_agreement(fp32, gpu):
     sub = genomes[:: 997]
     assert np.array_equal(gpu.run(hb.BatchRequest(1, sub, 1000)).results,
                           O.simulate_batch(1, sub, 1000).results)
+
+
+def test_fp32_blowup_and_precision_switch(fp32):
+    """A multi-body blow-up is reported at the same step as the reference
+    (the check is the same |x| <= 1e6 test), and switching a context between
+    precisions takes effect on the next call (FP64 = bit-exact again)."""
+    kind = 1
+    seeds = np.array([5, 3, 9, 1], dtype=np.uint64)
+    soa = hb.build_states(kind, seeds)
+    n = 2
+    pos = soa[: 3 * n].T.reshape(4, n, 3)
+    vel = soa[3 * n: 6 * n].T.reshape(4, n, 3).copy()
+    rest = soa[6 * n:].T
+    vel[1, 0, 2] = 1e9
+    vel[3, 1, 2] = 1e9
+    _, fail, _, _ = fp32.run_states(kind, pos, vel, rest, steps=50, seeds=seeds)
+    assert list(fail) == [0, 1, 0, 1]
+    sub = np.arange(256, dtype=np.uint64)
+    fp32.ctx.set_precision(_lib.HB_PRECISION_FP64)
+    try:
+        assert np.array_equal(fp32.run(hb.BatchRequest(2, sub, 200)).results,
+                              O.simulate_batch(2, sub, 200).results)
+    finally:
+        fp32.ctx.set_precision(_lib.HB_PRECISION_FP32)
+    with pytest.raises(Exception):
+        fp32.ctx.set_precision(7)
