@@ -16,6 +16,8 @@
 // order, is re-sorted by (low 32 bits descending, index ascending) —
 // insertion sort by the run's first thread; runs are a few elements (two
 // fitness values agree in their top 32 bits ~2^-20 relative apart).
+#include <atomic>
+
 #include <cooperative_groups.h>
 #include <cub/block/block_radix_rank.cuh>
 #include <cub/device/device_radix_sort.cuh>
@@ -225,12 +227,17 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
 
 cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
                                 cudaStream_t st) {
-    static bool attr_done = false;  // per process; the attribute is per function
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(sizeof(SortSmem)));
+    // the >48 KB dynamic shared-memory opt-in, once per device
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(done.load() & bit)) {
+        e = cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sizeof(SortSmem)));
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        done.fetch_or(bit);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(kSortCtas);
