@@ -160,8 +160,9 @@ def run_ea_native(kind: ModelKind, population_size: int, generations: int, steps
         times = np.ascontiguousarray(device_times, dtype=np.float64)
     elif isinstance(executor, MultiGpuExecutor) and executor.shares is not None:
         times = None
-    gen = np.empty(population_size, dtype=np.uint64)
-    fit = np.empty(population_size)
+    # page-locked (recycled) outputs: the final population is DMA'd straight in
+    gen = _lib.pinned.empty(population_size, np.uint64)
+    fit = _lib.pinned.empty(population_size, np.float64)
     best = C.c_double(0)
     prof = _lib.PhaseProfile()
     hg = hf = None
