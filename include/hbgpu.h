@@ -263,10 +263,11 @@ hb_status hb_ea_select_vary(hb_ctx* ctx, const uint64_t* d_genomes, const double
                             size_t pop, uint64_t g, uint64_t* d_next, double* d_next_fitness);
 
 /* ---- fast-path self test ----------------------------------------------------
- * Evaluates the kernels' branch-free sqrt(x[i]) and x[i] / y[i] replicas and
- * the library IEEE versions on the device.  Counts operands where the replica
- * claims validity but differs in any bit (must be 0), and operands the
- * replica flags for exact replay. */
+ * Evaluates the kernels' branch-free sqrt(x[i]) replica and their certified
+ * division x[i] / RN(sqrt(y[i]^2)) (the reciprocal taken from the sqrt's
+ * refined rsqrt, as in the projection) against the library IEEE versions on
+ * the device.  Counts operands where the fast path claims validity but
+ * differs in any bit (must be 0), and operands it flags for exact replay. */
 hb_status hb_check_fast_math(hb_ctx* ctx, const double* x, const double* y, size_t n,
                              uint64_t* sqrt_mismatch, uint64_t* div_mismatch,
                              uint64_t* sqrt_flagged, uint64_t* div_flagged);
