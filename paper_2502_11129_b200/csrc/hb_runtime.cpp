@@ -306,6 +306,7 @@ struct hb_ctx {
     uint64_t* h_fail = nullptr;
     size_t h_n_cap = 0;
     unsigned* h_count = nullptr;
+    unsigned* h_count_dev = nullptr;  // device address of the mapped h_count
     unsigned long long* d_ops = nullptr;  // Box executed-work counter (running total)
 
     // the batch currently resident on the device
@@ -609,6 +610,11 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
         delete c;
         return set_global(HB_CUDA_ERROR, "stream/scratch creation failed");
     }
+    c->h_count_dev = static_cast<unsigned*>(mapped_device_ptr(c->h_count));
+    if (!c->h_count_dev) {
+        hb_ctx_destroy(c);
+        return set_global(HB_CUDA_ERROR, "mapped counter has no device address");
+    }
     *out = c;
     return HB_OK;
 }
@@ -730,9 +736,9 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
     }
     volatile unsigned* flag = reinterpret_cast<volatile unsigned*>(c->h_count + 2);
     *flag = 0u;
-    void* dflag = mapped_device_ptr(c->h_count);
+    unsigned* dflag = c->h_count_dev;
     hb::SimArgs a{nullptr, dseeds, n, n, steps, hb::kSimDt, dout, c->d_fail, c->d_count, nullptr,
-                  reinterpret_cast<volatile unsigned*>(static_cast<unsigned*>(dflag) + 2), c->d_ops};
+                  reinterpret_cast<volatile unsigned*>(dflag + 2), c->d_ops};
     c->staged_kind = -1;
     tr.mark("args");
     HB_TRY(c->cuda(launch_kernel(c, hb::Box, a), "kernel launch"));
