@@ -562,8 +562,13 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
                                 "offspring slices evaluated per rank, NCCL fitness all-gather, "
                                 "identical device selection on every rank; final population D2H)"},
                 "evaluation_fraction": ev / tot if tot else None,
+                "phases_ms_per_run": {k: 1e3 * sum(getattr(p, k + "_s") for p in profs) / a.steps
+                                      for k in ("selection", "evaluation", "bookkeeping", "total")},
                 "best_fitness": r.best_fitness, "clocks": clk,
-                "gpu_launches": a.steps * (G + 1) * (1 if ws == 1 else 1),
+                # per run: genome init; per evaluation the simulation + fitness
+                # gather; per generation the selection (cluster sort, tie fix,
+                # select/vary, + the graph's generation bump on one GPU)
+                "gpu_launches": a.steps * (1 + 2 * (G + 1) + (4 if ws == 1 else 3) * G),
                 "parity": "genomes + fitness bit-identical to reference run_ea"}
         print(json.dumps(line))
     ex.ctx.close()

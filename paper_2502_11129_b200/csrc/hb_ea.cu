@@ -17,6 +17,7 @@
 // insertion sort by the run's first thread; runs are a few elements (two
 // fitness values agree in their top 32 bits ~2^-20 relative apart).
 #include <atomic>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 #include <cub/block/block_radix_rank.cuh>
@@ -31,9 +32,10 @@ namespace hb {
 
 namespace {
 
-__global__ void init_genomes_kernel(uint64_t key, size_t pop, uint64_t* genomes) {
+__global__ void init_genomes_kernel(uint64_t key, size_t pop, uint64_t* genomes, uint64_t* g_dev) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i < pop) genomes[i] = rng_at(key, i);
+    if (g_dev && i == 0) *g_dev = 1;  // the first generation of the loop
 }
 
 // (high word of fitness[i], i)
@@ -107,8 +109,10 @@ unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
 // ---------------------------------------------------------------------------
 // One-cluster radix sort of up to 65 536 (high word, index) pairs: the
-// stable 4-pass LSD sort of the selection in a single launch.  8 CTAs of
-// 1 024 threads (a portable cluster) each hold an 8 192-item tile in shared
+// stable 4-pass LSD sort of the selection in a single launch.  CTAS CTAs of
+// 1 024 threads form one cluster (16, non-portable, where the device can
+// schedule it — half the items per SM of the portable 8 and the pass time
+// is issue-bound per SM — else 8); each holds a 1 024 x ITEMS tile in shared
 // memory; per 8-bit digit pass every CTA ranks its tile stably
 // (cub::BlockRadixRankMatch), the CTAs exchange their digit histograms through
 // distributed shared memory, and every item is scattered straight into its
@@ -117,15 +121,15 @@ unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 // key and higher indices, so it ends up after every real item.  Replaces the
 // ~20 launches of the device-wide sort (the passes are latency-bound at
 // this size).
-constexpr int kSortCtas = 8, kSortThreads = 1024, kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;  // 8 192
-constexpr int kSortMax = kSortCtas * kSortTile;       // 65 536
+constexpr int kSortThreads = 1024;
+constexpr int kSortMax = 65536;
 using SortRank = cub::BlockRadixRankMatch<kSortThreads, 8, false>;  // match.any ranking: small per-warp counters
 
+template <int ITEMS>
 struct SortSmem {
-    uint2 buf[kSortTile];  // (key, index): every CTA has read its tile into registers
-                           // before the histogram barrier, so the scatter after
-                           // it may overwrite the tile in place
+    uint2 buf[kSortThreads * ITEMS];  // (key, index): every CTA has read its tile into
+                                      // registers before the histogram barrier, so the
+                                      // scatter after it may overwrite the tile in place
     typename SortRank::TempStorage rank;
     int hist[256];    // this CTA's digit counts (read by the whole cluster)
     int prefix[256];  // this CTA's exclusive digit prefix
@@ -138,37 +142,40 @@ struct DigitAt {
     __device__ __forceinline__ uint32_t Digit(uint32_t k) const { return (k >> shift) & 0xffu; }
 };
 
+template <int CTAS>
 __global__ void __launch_bounds__(kSortThreads)
 cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out) {
+    constexpr int ITEMS = kSortMax / (CTAS * kSortThreads);
+    constexpr int TILE = kSortThreads * ITEMS;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+    SortSmem<ITEMS>& sm = *reinterpret_cast<SortSmem<ITEMS>*>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
     const int c = static_cast<int>(cluster.block_rank());
     const int t = threadIdx.x;
     // warp-striped: item j of lane l in warp w is tile position w*32*K + 32j + l —
     // the order BlockRadixRankMatch ranks ties in (warp, item, lane), so the
     // ranking is stable with respect to tile order
-    const int stripe = (t >> 5) * 32 * kSortItems + (t & 31);
-    uint32_t key[kSortItems], idx[kSortItems];
+    const int stripe = (t >> 5) * 32 * ITEMS + (t & 31);
+    uint32_t key[ITEMS], idx[ITEMS];
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const int e = c * kSortTile + stripe + 32 * j;
+    for (int j = 0; j < ITEMS; ++j) {
+        const int e = c * TILE + stripe + 32 * j;
         idx[j] = static_cast<uint32_t>(e);
         key[j] = e < n ? ~static_cast<uint32_t>(__double2hiint(fitness[e])) : 0xffffffffu;
     }
     for (int pass = 0; pass < 4; ++pass) {
-        int ranks[kSortItems];
+        int ranks[ITEMS];
         int excl[1];
         SortRank(sm.rank).RankKeys(key, ranks, DigitAt{8u * pass}, excl);
         if (t < 256) sm.prefix[t] = excl[0];
         __syncthreads();
-        if (t < 256) sm.hist[t] = (t < 255 ? sm.prefix[t + 1] : kSortTile) - sm.prefix[t];
+        if (t < 256) sm.hist[t] = (t < 255 ? sm.prefix[t + 1] : TILE) - sm.prefix[t];
         cluster.sync();  // every CTA's histogram is visible
         if (t < 256) {
             int tot = 0, before = 0;
 #pragma unroll
-            for (int r = 0; r < kSortCtas; ++r) {
+            for (int r = 0; r < CTAS; ++r) {
                 const int v = cluster.map_shared_rank(sm.hist, r)[t];
                 tot += v;
                 before += r < c ? v : 0;
@@ -195,28 +202,28 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
         uint2* next = sm.buf;
         const uint32_t next_sa = static_cast<uint32_t>(__cvta_generic_to_shared(next));
 #pragma unroll
-        for (int j = 0; j < kSortItems; ++j) {
+        for (int j = 0; j < ITEMS; ++j) {
             const uint32_t d = (key[j] >> (8 * pass)) & 0xffu;
             const int pos = sm.goff[d] + ranks[j] - sm.prefix[d];
             // st.shared::cluster into the destination CTA's tile (mapa: the
             // same shared-window offset in CTA pos / tile)
-            const uint32_t local = next_sa + static_cast<uint32_t>(pos % kSortTile) * 8u;
+            const uint32_t local = next_sa + static_cast<uint32_t>(pos % TILE) * 8u;
             uint32_t remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(pos / kSortTile));
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(pos / TILE));
             asm volatile("st.shared::cluster.v2.u32 [%0], {%1, %2};" :: "r"(remote), "r"(key[j]), "r"(idx[j])
                          : "memory");
         }
         cluster.sync();  // every item has arrived in its tile
 #pragma unroll
-        for (int j = 0; j < kSortItems; ++j) {
+        for (int j = 0; j < ITEMS; ++j) {
             const uint2 kv = next[stripe + 32 * j];
             key[j] = kv.x;
             idx[j] = kv.y;
         }
     }
 #pragma unroll
-    for (int j = 0; j < kSortItems; ++j) {
-        const int p = c * kSortTile + stripe + 32 * j;
+    for (int j = 0; j < ITEMS; ++j) {
+        const int p = c * TILE + stripe + 32 * j;
         if (p < n) {
             key_out[p] = ~key[j];
             idx_out[p] = idx[j];
@@ -225,40 +232,74 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
     cluster.sync();  // no CTA leaves while another may still read its shared memory
 }
 
-cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
-                                cudaStream_t st) {
-    // the >48 KB dynamic shared-memory opt-in, once per device
-    static std::atomic<uint64_t> done{0};
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(done.load() & bit)) {
-        e = cudaFuncSetAttribute(cluster_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sizeof(SortSmem)));
-        if (e != cudaSuccess) return e;
-        done.fetch_or(bit);
-    }
+template <int CTAS>
+cudaLaunchConfig_t sort_config(cudaStream_t st, cudaLaunchAttribute* attr) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kSortCtas);
+    cfg.gridDim = dim3(CTAS);
     cfg.blockDim = dim3(kSortThreads);
-    cfg.dynamicSmemBytes = sizeof(SortSmem);
+    cfg.dynamicSmemBytes = sizeof(SortSmem<kSortMax / (CTAS * kSortThreads)>);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kSortCtas;
+    attr[0].val.clusterDim.x = CTAS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, cluster_sort_kernel, fitness, n, key_out, idx_out);
+    return cfg;
+}
+
+// Per device, once: the >48 KB dynamic shared-memory opt-in for both
+// variants, the non-portable cluster opt-in, and whether a 16-CTA cluster of
+// this kernel fits the device (cudaOccupancyMaxActiveClusters).  State bits:
+// 1 = probed, 2 = 16-CTA cluster usable.
+int sort_cluster_ctas(int dev, cudaStream_t st, cudaError_t* err) {
+    static std::atomic<uint8_t> state[64];
+    uint8_t s = state[dev & 63].load();
+    if (!(s & 1)) {
+        *err = cudaFuncSetAttribute(cluster_sort_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(sizeof(SortSmem<kSortMax / (8 * kSortThreads)>)));
+        if (*err != cudaSuccess) return 0;
+        bool wide = getenv("HB_SORT_CLUSTER8") == nullptr;
+        if (wide) {
+            wide = cudaFuncSetAttribute(cluster_sort_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(sizeof(SortSmem<kSortMax / (16 * kSortThreads)>))) ==
+                       cudaSuccess &&
+                   cudaFuncSetAttribute(cluster_sort_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                        1) == cudaSuccess;
+            int clusters = 0;
+            cudaLaunchAttribute attr[1];
+            cudaLaunchConfig_t cfg = sort_config<16>(st, attr);
+            wide = wide && cudaOccupancyMaxActiveClusters(&clusters, cluster_sort_kernel<16>, &cfg) == cudaSuccess &&
+                   clusters >= 1;
+            cudaGetLastError();  // a refused probe is not an error of this call
+        }
+        s = static_cast<uint8_t>(1 | (wide ? 2 : 0));
+        state[dev & 63].store(s);
+    }
+    return (s & 2) ? 16 : 8;
+}
+
+cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
+                                cudaStream_t st) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const int ctas = sort_cluster_ctas(dev, st, &e);
+    if (ctas == 0) return e;
+    cudaLaunchAttribute attr[1];
+    if (ctas == 16) {
+        cudaLaunchConfig_t cfg = sort_config<16>(st, attr);
+        return cudaLaunchKernelEx(&cfg, cluster_sort_kernel<16>, fitness, n, key_out, idx_out);
+    }
+    cudaLaunchConfig_t cfg = sort_config<8>(st, attr);
+    return cudaLaunchKernelEx(&cfg, cluster_sort_kernel<8>, fitness, n, key_out, idx_out);
 }
 
 }  // namespace
 
-cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st) {
+cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st, uint64_t* g_dev) {
     if (pop == 0) return cudaSuccess;
-    init_genomes_kernel<<<blocks_for(pop), 256, 0, st>>>(seed ^ kInitKey, pop, d_genomes);
+    init_genomes_kernel<<<blocks_for(pop), 256, 0, st>>>(seed ^ kInitKey, pop, d_genomes, g_dev);
     return cudaGetLastError();
 }
 

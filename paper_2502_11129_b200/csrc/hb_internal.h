@@ -58,7 +58,9 @@ cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, do
                                   double* o2, double* o3, unsigned char* flags, cudaStream_t st);
 
 // Generation loop helpers (hb_ea.cu).
-cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st);
+// g_dev (optional): the graph-replayed loop's generation counter, set to 1
+cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st,
+                            uint64_t* g_dev = nullptr);
 cudaError_t ea_fitness_from_results(const hb_variant_result* out, size_t n, double* fitness,
                                     cudaStream_t st);
 size_t ea_select_scratch_bytes(size_t pop);

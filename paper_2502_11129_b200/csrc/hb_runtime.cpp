@@ -294,6 +294,7 @@ struct hb_ctx {
     uint64_t* h_ea_gen = nullptr;  // pinned staging of the final population
     double* h_ea_fit = nullptr;
     cudaEvent_t ea_ev[3] = {nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> ea_timing;  // per-generation selection brackets of the queued loop
     cudaGraphExec_t ea_graph[2] = {nullptr, nullptr};  // select/vary cur -> cur ^ 1, for d_ea_pop_cap
     size_t ea_graph_pop = 0;
     uint64_t* d_ea_g = nullptr;  // generation counter the graphs read and advance
@@ -631,6 +632,7 @@ void hb_ctx_destroy(hb_ctx* c) {
     cudaFree(c->d_ea_scratch);
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
     for (cudaEvent_t e : c->ea_ev) if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ea_timing) cudaEventDestroy(e);
     for (cudaGraphExec_t g : c->ea_graph) if (g) cudaGraphExecDestroy(g);
     cudaFree(c->d_ea_g);
     cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
@@ -1062,12 +1064,30 @@ std::string batch_failure_text(const uint64_t* seeds, const uint64_t* fail, size
     return msg + ": " + failed.front().second;
 }
 
+// The sequential std::max fold of ea.cpp:101-103 (the first of equal maxima,
+// e.g. +0 before -0; a NaN first element stays) without its one dependent
+// chain: eight independent running maxima, then the first element equal to
+// the maximum.
+double best_fitness(const double* f, size_t n) {
+    double m[8];
+    for (double& v : m) v = f[0];
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8)
+        for (int k = 0; k < 8; ++k) m[k] = f[i + k] > m[k] ? f[i + k] : m[k];
+    for (; i < n; ++i) m[0] = f[i] > m[0] ? f[i] : m[0];
+    double mx = m[0];
+    for (int k = 1; k < 8; ++k) mx = m[k] > mx ? m[k] : mx;
+    for (size_t j = 0; j < n; ++j)
+        if (f[j] == mx) return f[j];
+    return f[0];
+}
+
 // Launch the simulation of n device-resident seeds on c's device; fitness
 // lands in d_fitness (c's device).  Models initialised on the host take the
 // seeds through the host initialiser first (blocking).  Counters are read
 // back asynchronously; eval_finish synchronises and checks them.
 hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uint64_t steps,
-                     double* d_fitness) {
+                     double* d_fitness, bool read_counts = true) {
     const bool dev_init = init_on_device(c, kind);
     HB_TRY(ensure_capacity(c, kind, n, !dev_init));
     if (!dev_init) {
@@ -1089,8 +1109,9 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
                   c->d_out, c->d_fail, c->d_count, nullptr, nullptr, c->d_ops};
     HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
     HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
-    HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
-                                   c->stream), "D2H count"));
+    if (read_counts)
+        HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                       c->stream), "D2H count"));
     return HB_OK;
 }
 
@@ -1276,11 +1297,6 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
                             "capture select/vary"));
         c0->ea_graph_pop = pop;
     }
-    {
-        static const uint64_t kFirstGeneration = 1;
-        HB_TRY(c0->cuda(cudaMemcpyAsync(c0->d_ea_g, &kFirstGeneration, sizeof(uint64_t),
-                                        cudaMemcpyHostToDevice, c0->stream), "H2D g"));
-    }
     cudaEvent_t ev_ready = c0->ea_ev[0], e0 = c0->ea_ev[1], e2 = c0->ea_ev[2];
 
     std::vector<double> times(count, 1.0);
@@ -1301,9 +1317,70 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
         return c0->cuda(cudaStreamSynchronize(c0->stream), "sync");
     };
 
+    // One device, seeds initialised on the device, no history requested: the
+    // whole loop is queued on the stream with no host round trip per
+    // generation.  The failure counter is not reset between evaluations, so
+    // one read at the end covers all of them; a blow-up anywhere falls through
+    // to the checked loop below, which re-runs from generation 0
+    // (deterministic) and throws at the first failing batch exactly like
+    // ea.cpp:81-82.
+    if (count == 1 && !history_genomes && !history_fitness && init_on_device(c0, kind)) {
+        const size_t n_ev = 2 * generations + 2;
+        while (c0->ea_timing.size() < n_ev) {
+            cudaEvent_t ev;
+            HB_TRY(c0->cuda(cudaEventCreate(&ev), "event"));
+            c0->ea_timing.push_back(ev);
+        }
+        cudaEvent_t* tev = c0->ea_timing.data();
+        cudaEventRecord(tev[0], c0->stream);
+        HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream, c0->d_ea_g), "init genomes"));
+        HB_TRY(eval_start(c0, kind, d_gen[0], pop, steps, d_fit[0], false));
+        int q = 0;
+        for (uint64_t g = 1; g <= generations; ++g) {
+            const int nxt = q ^ 1;
+            cudaEventRecord(tev[2 * g], c0->stream);
+            HB_TRY(c0->cuda(cudaGraphLaunch(c0->ea_graph[q], c0->stream), "select/vary"));
+            cudaEventRecord(tev[2 * g + 1], c0->stream);
+            HB_TRY(eval_start(c0, kind, d_gen[nxt] + mu, mu, steps, d_fit[nxt] + mu, false));
+            q = nxt;
+        }
+        cudaEventRecord(tev[1], c0->stream);
+        HB_TRY(c0->cuda(cudaMemcpyAsync(c0->h_count, c0->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                        c0->stream), "D2H count"));
+        const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
+        HB_TRY(c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[q], pop * sizeof(uint64_t),
+                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
+        HB_TRY(c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[q], pop * sizeof(double),
+                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
+        HB_TRY(c0->cuda(cudaStreamSynchronize(c0->stream), "sync"));
+        c0->last_failed = c0->h_count[0];
+        c0->last_replays = c0->h_count[1];
+        c0->counters_dirty = (c0->h_count[0] | c0->h_count[1]) != 0;
+        if (c0->h_count[0] == 0) {
+            if (!pg) std::memcpy(genomes_out, c0->h_ea_gen, pop * sizeof(uint64_t));
+            if (!pf) std::memcpy(fitness_out, c0->h_ea_fit, pop * sizeof(double));
+            if (best_out) {
+                *best_out = best_fitness(fitness_out, pop);
+            }
+            float ms = 0.f;
+            double sel = 0.0;
+            for (uint64_t g = 1; g <= generations; ++g) {
+                cudaEventElapsedTime(&ms, tev[2 * g], tev[2 * g + 1]);
+                sel += 1e-3 * ms;
+            }
+            cudaEventElapsedTime(&ms, tev[0], tev[1]);
+            prof.total_s = elapsed_s(t_start);
+            prof.selection_s = std::min(sel, prof.total_s);
+            prof.evaluation_s = std::min(std::max(1e-3 * ms - sel, 0.0), prof.total_s - prof.selection_s);
+            prof.bookkeeping_s = prof.total_s - prof.selection_s - prof.evaluation_s;
+            if (profile) *profile = prof;
+            return HB_OK;
+        }
+    }
+
     // initial population + evaluation (ea.cpp:48-54)
     auto tb = clk::now();
-    HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream), "init genomes"));
+    HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream, c0->d_ea_g), "init genomes"));
     cudaEventRecord(ev_ready, c0->stream);
     prof.bookkeeping_s += elapsed_s(tb);
     auto te = clk::now();
@@ -1351,9 +1428,7 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     }
     prof.bookkeeping_s += elapsed_s(tb);
     if (best_out) {
-        double best = fitness_out[0];
-        for (size_t i = 1; i < pop; ++i) best = std::max(best, fitness_out[i]);  // ea.cpp:101-103
-        *best_out = best;
+        *best_out = best_fitness(fitness_out, pop);
     }
     prof.total_s = elapsed_s(t_start);
     // the device time of selection+variation is reported as selection (one
