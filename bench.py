@@ -566,9 +566,9 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
                                       for k in ("selection", "evaluation", "bookkeeping", "total")},
                 "best_fitness": r.best_fitness, "clocks": clk,
                 # per run: genome init; per evaluation the simulation + fitness
-                # gather; per generation the selection (cluster sort, tie fix,
-                # select/vary, + the graph's generation bump on one GPU)
-                "gpu_launches": a.steps * (1 + 2 * (G + 1) + (4 if ws == 1 else 3) * G),
+                # gather; per generation the selection (cluster sort, then tie
+                # fix + select + offspring in one kernel)
+                "gpu_launches": a.steps * (1 + 2 * (G + 1) + 2 * G),
                 "parity": "genomes + fitness bit-identical to reference run_ea"}
         print(json.dumps(line))
     ex.ctx.close()

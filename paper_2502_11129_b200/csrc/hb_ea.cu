@@ -11,13 +11,14 @@
 // positive finite double for every completed variant (a blown-up variant
 // aborts the generation, as batch_failure aborts run_ea), so the order of
 // the IEEE bit patterns is the numeric order.  The sort runs on the high 32
-// bits only (a stable 4-pass radix sort of (hi32, index) — half the passes
-// of a 64-bit key), then every run of equal high words, already in index
+// bits only (a stable radix sort of (hi32, index), at most 4 passes — half
+// those of a 64-bit key), then every run of equal high words, already in index
 // order, is re-sorted by (low 32 bits descending, index ascending) —
 // insertion sort by the run's first thread; runs are a few elements (two
 // fitness values agree in their top 32 bits ~2^-20 relative apart).
 #include <atomic>
 #include <cstdlib>
+#include <string>
 
 #include <cooperative_groups.h>
 #include <cub/block/block_radix_rank.cuh>
@@ -35,27 +36,36 @@ namespace {
 __global__ void init_genomes_kernel(uint64_t key, size_t pop, uint64_t* genomes, uint64_t* g_dev) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     if (i < pop) genomes[i] = rng_at(key, i);
-    if (g_dev && i == 0) *g_dev = 1;  // the first generation of the loop
+    if (g_dev && i == 0) *g_dev = 0;  // each selection's first kernel advances it (to 1 first)
 }
 
 // (high word of fitness[i], i)
-__global__ void key_hi_kernel(const double* fitness, size_t n, uint32_t* key, uint32_t* idx) {
+__global__ void key_hi_kernel(const double* fitness, size_t n, uint32_t* key, uint32_t* idx, uint64_t* g_dev) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    if (g_dev && i == 0) *g_dev += 1;  // this generation's index (read by tie_select_kernel)
     if (i >= n) return;
     key[i] = static_cast<uint32_t>(__double2hiint(fitness[i]));
     idx[i] = static_cast<uint32_t>(i);
 }
 
-// Within each run of equal high words (index order after the stable sort),
-// order by low word descending, index ascending: the run's first position
-// insertion-sorts it.
-__global__ void tie_fix_kernel(const double* fitness, const uint32_t* key, size_t n, uint32_t* order) {
+// Tie fix, selection and variation in one pass over the sorted order
+// (ea.cpp:60-79).  The sort ordered (high word desc, index asc); within a run
+// of equal high words the order must be low word descending, index
+// ascending: the run's first position insertion-sorts the whole run (it may
+// reach past mu) and emits, for the run's positions q < mu, parent
+// next[q] = genomes[order[q]] with its fitness and offspring
+// next[mu + q] = rng_at(parent ^ kChildKey, (g << 32) + q).  Runs are
+// almost always of one, so each thread emits its own position (coalesced).
+// g from *g_dev when given (graph replays; advanced by the sort kernel).
+__global__ void tie_select_kernel(const uint64_t* genomes, const double* fitness, const uint32_t* key,
+                                  size_t n, uint32_t* order, size_t mu, uint64_t g, const uint64_t* g_dev,
+                                  uint64_t* next, double* next_fit) {
     const size_t p = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (p >= n) return;
-    if (p > 0 && key[p - 1] == key[p]) return;        // not a run start
-    if (p + 1 >= n || key[p + 1] != key[p]) return;    // run of one
+    if (p >= mu) return;
+    const uint32_t kp = key[p];
+    if (p > 0 && key[p - 1] == kp) return;  // inside a run: its first position emits it
     size_t end = p + 1;
-    while (end < n && key[end] == key[p]) ++end;
+    while (end < n && key[end] == kp) ++end;
     for (size_t a = p + 1; a < end; ++a) {
         const uint32_t ia = order[a];
         const uint32_t la = static_cast<uint32_t>(__double2loint(fitness[ia]));
@@ -69,36 +79,16 @@ __global__ void tie_fix_kernel(const double* fitness, const uint32_t* key, size_
         }
         order[b] = ia;
     }
+    const uint64_t gen = g_dev ? *g_dev : g;
+    const size_t stop = end < mu ? end : mu;
+    for (size_t q = p; q < stop; ++q) {
+        const uint32_t o = order[q];
+        const uint64_t parent = genomes[o];
+        next[q] = parent;
+        next_fit[q] = fitness[o];
+        next[mu + q] = rng_at(parent ^ kChildKey, (gen << 32) + q);
+    }
 }
-
-// next[0, mu) = parents (genomes[order[i]]), next_fit[0, mu) = their fitness;
-// next[mu + i] = offspring of parent i.
-__global__ void select_vary_kernel(const uint64_t* genomes, const double* fitness,
-                                   const uint32_t* order, size_t mu, uint64_t g,
-                                   uint64_t* next, double* next_fit) {
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= mu) return;
-    const uint64_t parent = genomes[order[i]];
-    next[i] = parent;
-    next_fit[i] = fitness[order[i]];
-    next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
-}
-
-// The generation index from device memory (graph replays read the counter
-// the previous replay advanced).
-__global__ void select_vary_dev_g_kernel(const uint64_t* genomes, const double* fitness,
-                                         const uint32_t* order, size_t mu, const uint64_t* g_dev,
-                                         uint64_t* next, double* next_fit) {
-    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
-    if (i >= mu) return;
-    const uint64_t g = *g_dev;
-    const uint64_t parent = genomes[order[i]];
-    next[i] = parent;
-    next_fit[i] = fitness[order[i]];
-    next[mu + i] = rng_at(parent ^ kChildKey, (g << 32) + i);
-}
-
-__global__ void bump_kernel(uint64_t* g_dev) { *g_dev += 1; }
 
 __global__ void fitness_from_results_kernel(const hb_variant_result* out, size_t n, double* fitness) {
     const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
@@ -121,20 +111,23 @@ unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 // key and higher indices, so it ends up after every real item.  Replaces the
 // ~20 launches of the device-wide sort (the passes are latency-bound at
 // this size).
-constexpr int kSortThreads = 1024;
 constexpr int kSortMax = 65536;
-using SortRank = cub::BlockRadixRankMatch<kSortThreads, 8, false>;  // match.any ranking: small per-warp counters
+template <int THREADS>
+using SortRank = cub::BlockRadixRankMatch<THREADS, 8, false>;  // match.any ranking: small per-warp counters
 
-template <int ITEMS>
+template <int THREADS, int ITEMS>
 struct SortSmem {
-    uint2 buf[kSortThreads * ITEMS];  // (key, index): every CTA has read its tile into
+    uint2 buf[THREADS * ITEMS];  // (key, index): every CTA has read its tile into
                                       // registers before the histogram barrier, so the
                                       // scatter after it may overwrite the tile in place
-    typename SortRank::TempStorage rank;
+    typename SortRank<THREADS>::TempStorage rank;
     int hist[256];    // this CTA's digit counts (read by the whole cluster)
     int prefix[256];  // this CTA's exclusive digit prefix
     int goff[256];    // global start of this CTA's items of each digit
     int tot[256];
+    uint32_t wor[32], wand[32];  // OR / AND of each warp's keys (which digits vary at all)
+    uint32_t kor, kand;          // ... of this CTA's keys
+    uint32_t vary;               // the cluster's varying key bits
 };
 
 struct DigitAt {
@@ -142,17 +135,18 @@ struct DigitAt {
     __device__ __forceinline__ uint32_t Digit(uint32_t k) const { return (k >> shift) & 0xffu; }
 };
 
-template <int CTAS>
-__global__ void __launch_bounds__(kSortThreads)
-cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out) {
-    constexpr int ITEMS = kSortMax / (CTAS * kSortThreads);
-    constexpr int TILE = kSortThreads * ITEMS;
+template <int CTAS, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1)
+cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out, uint64_t* g_dev) {
+    constexpr int ITEMS = kSortMax / (CTAS * THREADS);
+    constexpr int TILE = THREADS * ITEMS;
     namespace cg = cooperative_groups;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmem<ITEMS>& sm = *reinterpret_cast<SortSmem<ITEMS>*>(smem_raw);
+    SortSmem<THREADS, ITEMS>& sm = *reinterpret_cast<SortSmem<THREADS, ITEMS>*>(smem_raw);
     cg::cluster_group cluster = cg::this_cluster();
     const int c = static_cast<int>(cluster.block_rank());
     const int t = threadIdx.x;
+    if (g_dev && c == 0 && t == 0) *g_dev += 1;  // this generation's index (read by tie_select_kernel)
     // warp-striped: item j of lane l in warp w is tile position w*32*K + 32j + l —
     // the order BlockRadixRankMatch ranks ties in (warp, item, lane), so the
     // ranking is stable with respect to tile order
@@ -164,14 +158,53 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
         idx[j] = static_cast<uint32_t>(e);
         key[j] = e < n ? ~static_cast<uint32_t>(__double2hiint(fitness[e])) : 0xffffffffu;
     }
+    {
+        uint32_t o = 0u, a = 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j < ITEMS; ++j) {
+            if (static_cast<int>(idx[j]) < n) {  // padding (all-ones keys, the highest
+                o |= key[j];                     // indices) sorts last whatever digits
+                a &= key[j];                     // are skipped
+            }
+        }
+        o = __reduce_or_sync(0xffffffffu, o);
+        a = __reduce_and_sync(0xffffffffu, a);
+        if ((t & 31) == 0) {  // read after the barriers of the first pass
+            sm.wor[t >> 5] = o;
+            sm.wand[t >> 5] = a;
+        }
+    }
+#pragma unroll
     for (int pass = 0; pass < 4; ++pass) {
+        // a digit no key varies in permutes nothing (the pass is the stable
+        // identity): skip it — a non-negative fitness of narrow exponent range
+        // leaves the top byte constant (decided from pass 0's exchange)
+        if (pass > 0 && ((sm.vary >> (8 * pass)) & 0xffu) == 0u) continue;
+        const uint32_t shift = 8u * pass;
         int ranks[ITEMS];
         int excl[1];
-        SortRank(sm.rank).RankKeys(key, ranks, DigitAt{8u * pass}, excl);
+        SortRank<THREADS>(sm.rank).RankKeys(key, ranks, DigitAt{shift}, excl);
         if (t < 256) sm.prefix[t] = excl[0];
         __syncthreads();
         if (t < 256) sm.hist[t] = (t < 255 ? sm.prefix[t + 1] : TILE) - sm.prefix[t];
-        cluster.sync();  // every CTA's histogram is visible
+        if (shift == 0 && t < 32) {
+            const bool w = t < THREADS / 32;
+            const uint32_t o = __reduce_or_sync(0xffffffffu, w ? sm.wor[t] : 0u);
+            const uint32_t a = __reduce_and_sync(0xffffffffu, w ? sm.wand[t] : 0xffffffffu);
+            if (t == 0) {
+                sm.kor = o;
+                sm.kand = a;
+            }
+        }
+        cluster.sync();  // every CTA's histogram (and key OR / AND) is visible
+        if (shift == 0 && t == 0) {
+            uint32_t o = 0u, a = 0xffffffffu;
+            for (int r = 0; r < CTAS; ++r) {
+                o |= *cluster.map_shared_rank(&sm.kor, r);
+                a &= *cluster.map_shared_rank(&sm.kand, r);
+            }
+            sm.vary = o ^ a;
+        }
         if (t < 256) {
             int tot = 0, before = 0;
 #pragma unroll
@@ -203,7 +236,7 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
         const uint32_t next_sa = static_cast<uint32_t>(__cvta_generic_to_shared(next));
 #pragma unroll
         for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t d = (key[j] >> (8 * pass)) & 0xffu;
+            const uint32_t d = (key[j] >> shift) & 0xffu;
             const int pos = sm.goff[d] + ranks[j] - sm.prefix[d];
             // st.shared::cluster into the destination CTA's tile (mapa: the
             // same shared-window offset in CTA pos / tile)
@@ -232,67 +265,68 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
     cluster.sync();  // no CTA leaves while another may still read its shared memory
 }
 
-template <int CTAS>
-cudaLaunchConfig_t sort_config(cudaStream_t st, cudaLaunchAttribute* attr) {
+template <int CTAS, int THREADS>
+cudaError_t launch_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out, uint64_t* g_dev,
+                        cudaStream_t st, bool probe_only = false) {
+    constexpr size_t smem = sizeof(SortSmem<THREADS, kSortMax / (CTAS * THREADS)>);
+    auto* kern = cluster_sort_kernel<CTAS, THREADS>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CTAS);
-    cfg.blockDim = dim3(kSortThreads);
-    cfg.dynamicSmemBytes = sizeof(SortSmem<kSortMax / (CTAS * kSortThreads)>);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
+    cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CTAS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cfg;
-}
-
-// Per device, once: the >48 KB dynamic shared-memory opt-in for both
-// variants, the non-portable cluster opt-in, and whether a 16-CTA cluster of
-// this kernel fits the device (cudaOccupancyMaxActiveClusters).  State bits:
-// 1 = probed, 2 = 16-CTA cluster usable.
-int sort_cluster_ctas(int dev, cudaStream_t st, cudaError_t* err) {
-    static std::atomic<uint8_t> state[64];
-    uint8_t s = state[dev & 63].load();
-    if (!(s & 1)) {
-        *err = cudaFuncSetAttribute(cluster_sort_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(sizeof(SortSmem<kSortMax / (8 * kSortThreads)>)));
-        if (*err != cudaSuccess) return 0;
-        bool wide = getenv("HB_SORT_CLUSTER8") == nullptr;
-        if (wide) {
-            wide = cudaFuncSetAttribute(cluster_sort_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(sizeof(SortSmem<kSortMax / (16 * kSortThreads)>))) ==
-                       cudaSuccess &&
-                   cudaFuncSetAttribute(cluster_sort_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed,
-                                        1) == cudaSuccess;
-            int clusters = 0;
-            cudaLaunchAttribute attr[1];
-            cudaLaunchConfig_t cfg = sort_config<16>(st, attr);
-            wide = wide && cudaOccupancyMaxActiveClusters(&clusters, cluster_sort_kernel<16>, &cfg) == cudaSuccess &&
-                   clusters >= 1;
-            cudaGetLastError();  // a refused probe is not an error of this call
-        }
-        s = static_cast<uint8_t>(1 | (wide ? 2 : 0));
-        state[dev & 63].store(s);
+    if (probe_only) {  // opt-ins, and whether one cluster fits the device
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(smem));
+        if (e == cudaSuccess && CTAS > 8)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        int clusters = 0;
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&clusters, kern, &cfg);
+        if (e == cudaSuccess && clusters < 1) e = cudaErrorInvalidConfiguration;
+        return e;
     }
-    return (s & 2) ? 16 : 8;
+    return cudaLaunchKernelEx(&cfg, kern, fitness, n, key_out, idx_out, g_dev);
 }
 
+// The cluster shape, probed once per device: 16 CTAs of 512 threads
+// (non-portable cluster; half the items per SM of the portable shape, and
+// the pass time is issue-bound per SM) where the device schedules it, else
+// the portable 8 x 1 024.  HB_SORT_SHAPE=8x1024|16x512|16x1024 pins one.
+// State: 0 = unprobed, else shape index + 1.
 cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
-                                cudaStream_t st) {
+                                uint64_t* g_dev, cudaStream_t st) {
+    static std::atomic<uint8_t> state[64];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
-    const int ctas = sort_cluster_ctas(dev, st, &e);
-    if (ctas == 0) return e;
-    cudaLaunchAttribute attr[1];
-    if (ctas == 16) {
-        cudaLaunchConfig_t cfg = sort_config<16>(st, attr);
-        return cudaLaunchKernelEx(&cfg, cluster_sort_kernel<16>, fitness, n, key_out, idx_out);
+    uint8_t s = state[dev & 63].load();
+    if (s == 0) {
+        const char* pin = getenv("HB_SORT_SHAPE");
+        const std::string want = pin ? pin : "";
+        if ((want.empty() || want == "16x512") && launch_sort<16, 512>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess)
+            s = 2;
+        else if (want == "16x1024" && launch_sort<16, 1024>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess)
+            s = 3;
+        else {
+            cudaGetLastError();  // a refused probe is not an error of this call
+            e = launch_sort<8, 1024>(nullptr, 0, nullptr, nullptr, nullptr, st, true);
+            if (e != cudaSuccess) return e;
+            s = 1;
+        }
+        state[dev & 63].store(s);
     }
-    cudaLaunchConfig_t cfg = sort_config<8>(st, attr);
-    return cudaLaunchKernelEx(&cfg, cluster_sort_kernel<8>, fitness, n, key_out, idx_out);
+    switch (s) {
+        case 2: return launch_sort<16, 512>(fitness, n, key_out, idx_out, g_dev, st);
+        case 3: return launch_sort<16, 1024>(fitness, n, key_out, idx_out, g_dev, st);
+        default: return launch_sort<8, 1024>(fitness, n, key_out, idx_out, g_dev, st);
+    }
 }
 
 }  // namespace
@@ -342,23 +376,16 @@ cudaError_t select_vary_impl(const uint64_t* d_genomes, const double* d_fitness,
     uint32_t* idx_out = reinterpret_cast<uint32_t*>(base + al(temp) + 3 * words);
     cudaError_t e;
     if (pop <= static_cast<size_t>(kSortMax)) {  // one cluster, one launch
-        e = launch_cluster_sort(d_fitness, static_cast<int>(pop), key_out, idx_out, st);
+        e = launch_cluster_sort(d_fitness, static_cast<int>(pop), key_out, idx_out, g_dev, st);
     } else {
-        key_hi_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, pop, key_in, idx_in);
+        key_hi_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, pop, key_in, idx_in, g_dev);
         e = cub::DeviceRadixSort::SortPairsDescending(d_temp, temp, key_in, key_out, idx_in, idx_out,
                                                       static_cast<int>(pop), 0, 32, st);
     }
     if (e != cudaSuccess) return e;
-    tie_fix_kernel<<<blocks_for(pop), 256, 0, st>>>(d_fitness, key_out, pop, idx_out);
     const size_t mu = pop / 2;
-    if (g_dev) {
-        select_vary_dev_g_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, d_fitness, idx_out, mu, g_dev,
-                                                                 d_next, d_next_fit);
-        bump_kernel<<<1, 1, 0, st>>>(g_dev);
-    } else {
-        select_vary_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, d_fitness, idx_out, mu, g, d_next,
-                                                           d_next_fit);
-    }
+    tie_select_kernel<<<blocks_for(mu), 256, 0, st>>>(d_genomes, d_fitness, key_out, pop, idx_out, mu, g, g_dev,
+                                                      d_next, d_next_fit);
     return cudaGetLastError();
 }
 
@@ -371,10 +398,10 @@ cudaError_t ea_select_vary(const uint64_t* d_genomes, const double* d_fitness, s
                             scratch_bytes, st);
 }
 
-// The same selection + variation captured once as a CUDA graph (iota, the
-// radix sort's ~30 passes/launches, gather + offspring, counter bump) —
-// replays pay one launch instead of one per kernel.  g comes from *g_dev,
-// advanced by every replay.
+// The same selection + variation captured once as a CUDA graph (the cluster
+// sort + tie_select_kernel; above 65 536: key_hi + the device-wide radix
+// sort's passes + tie_select_kernel) — replays pay one launch instead of one
+// per kernel.  g comes from *g_dev, advanced by every replay's first kernel.
 cudaError_t ea_select_vary_graph(const uint64_t* d_genomes, const double* d_fitness, size_t pop,
                                  uint64_t* g_dev, uint64_t* d_next, double* d_next_fit, void* scratch,
                                  size_t scratch_bytes, cudaStream_t st, cudaGraphExec_t* exec) {

@@ -117,13 +117,16 @@ def test_device_sharded_ea_equals_reference_loop(world):
         assert np.array_equal(np.array(f), ref.population.fitnesses)
 
 
-@pytest.mark.parametrize("pop", [4096, 40002, 65536, 70000])
-def test_select_vary_ties_match_stable_sort(gpu, pop):
+@pytest.mark.parametrize("pop,shape", [(4096, "mixed"), (40002, "mixed"), (65536, "mixed"), (70000, "mixed"),
+                                       (4096, "sparse"), (40002, "sparse"), (65536, "sparse")])
+def test_select_vary_ties_match_stable_sort(gpu, pop, shape):
     """hb_ea_select_vary on crafted fitness: exact duplicates, +0, long runs of
     equal high words with different low words — parents and their order must
     be std::stable_sort with `>` (ea.cpp:60-72), offspring the reference hash.
     Populations below / at the cluster sort's 65 536 (partial and full tiles)
-    and above it (the device-wide sort)."""
+    and above it (the device-wide sort).  "sparse": high words whose top byte
+    and bits 8-15 are shared by every key, so the cluster sort skips those
+    digit passes (and bits 0-7 / 16-23 still order them)."""
     import ctypes as C
 
     import torch
@@ -137,8 +140,14 @@ def test_select_vary_ties_match_stable_sort(gpu, pop):
     sel = rng.random(pop) < 0.5
     bits[sel] = (hi_words[grp[sel]] << np.uint64(32)) | (bits[sel] & np.uint64(0xFFFFFFFF))
     fit = bits.view(np.float64).copy()
+    if shape == "sparse":  # hi = 0x3F r1 5A r0: positive, in [2^-15, 2)
+        hi = (np.uint64(0x3F005A00) | (rng.integers(0, 256, pop, dtype=np.uint64) << np.uint64(16))
+              | rng.integers(0, 256, pop, dtype=np.uint64))
+        hi[sel] = hi[grp[sel]]  # runs of shared high words
+        fit = ((hi << np.uint64(32)) | (bits & np.uint64(0xFFFFFFFF))).view(np.float64).copy()
+    else:
+        fit[:7] = 0.0                                                      # +0 fitness
     fit[rng.choice(pop, 300, replace=False)] = fit[rng.choice(pop, 300)]  # exact duplicates
-    fit[:7] = 0.0                                                          # +0 fitness
     fit[100:140] = fit[99]                                                 # a long exact tie run
     genomes = rng.integers(0, 2**63, pop, dtype=np.uint64)
     dev = torch.device("cuda", 0)
