@@ -295,6 +295,8 @@ struct hb_ctx {
     double* h_ea_fit = nullptr;
     cudaEvent_t ea_ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ea_timing;  // per-generation selection brackets of the queued loop
+    cudaStream_t ea_copy = nullptr;      // final-population D2H overlapping the last evaluation
+    cudaEvent_t ea_sel_done = nullptr;
     cudaGraphExec_t ea_graph[2] = {nullptr, nullptr};  // select/vary cur -> cur ^ 1, for d_ea_pop_cap
     size_t ea_graph_pop = 0;
     uint64_t* d_ea_g = nullptr;  // generation counter the graphs read and advance
@@ -633,6 +635,8 @@ void hb_ctx_destroy(hb_ctx* c) {
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
     for (cudaEvent_t e : c->ea_ev) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ea_timing) cudaEventDestroy(e);
+    if (c->ea_sel_done) cudaEventDestroy(c->ea_sel_done);
+    if (c->ea_copy) cudaStreamDestroy(c->ea_copy);
     for (cudaGraphExec_t g : c->ea_graph) if (g) cudaGraphExecDestroy(g);
     cudaFree(c->d_ea_g);
     cudaFreeHost(c->h_init); cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
@@ -1331,6 +1335,13 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
             HB_TRY(c0->cuda(cudaEventCreate(&ev), "event"));
             c0->ea_timing.push_back(ev);
         }
+        if (!c0->ea_copy) {
+            HB_TRY(c0->cuda(cudaStreamCreateWithFlags(&c0->ea_copy, cudaStreamNonBlocking), "stream"));
+            HB_TRY(c0->cuda(cudaEventCreateWithFlags(&c0->ea_sel_done, cudaEventDisableTiming), "event"));
+        }
+        const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
+        uint64_t* h_gen = pg ? genomes_out : c0->h_ea_gen;
+        double* h_fit = pf ? fitness_out : c0->h_ea_fit;
         cudaEvent_t* tev = c0->ea_timing.data();
         cudaEventRecord(tev[0], c0->stream);
         HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream, c0->d_ea_g), "init genomes"));
@@ -1341,18 +1352,24 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
             cudaEventRecord(tev[2 * g], c0->stream);
             HB_TRY(c0->cuda(cudaGraphLaunch(c0->ea_graph[q], c0->stream), "select/vary"));
             cudaEventRecord(tev[2 * g + 1], c0->stream);
+            if (g == generations) {  // the final genomes and parent fitness are known: copy them
+                cudaEventRecord(c0->ea_sel_done, c0->stream);  // out while the offspring evaluate
+                HB_TRY(c0->cuda(cudaStreamWaitEvent(c0->ea_copy, c0->ea_sel_done, 0), "wait"));
+                HB_TRY(c0->cuda(cudaMemcpyAsync(h_gen, d_gen[nxt], pop * sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                                                c0->ea_copy), "D2H"));
+                HB_TRY(c0->cuda(cudaMemcpyAsync(h_fit, d_fit[nxt], mu * sizeof(double), cudaMemcpyDeviceToHost,
+                                                c0->ea_copy), "D2H"));
+            }
             HB_TRY(eval_start(c0, kind, d_gen[nxt] + mu, mu, steps, d_fit[nxt] + mu, false));
             q = nxt;
         }
         cudaEventRecord(tev[1], c0->stream);
         HB_TRY(c0->cuda(cudaMemcpyAsync(c0->h_count, c0->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                         c0->stream), "D2H count"));
-        const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
-        HB_TRY(c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[q], pop * sizeof(uint64_t),
-                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
-        HB_TRY(c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[q], pop * sizeof(double),
-                                        cudaMemcpyDeviceToHost, c0->stream), "D2H"));
+        HB_TRY(c0->cuda(cudaMemcpyAsync(h_fit + mu, d_fit[q] + mu, mu * sizeof(double), cudaMemcpyDeviceToHost,
+                                        c0->stream), "D2H"));
         HB_TRY(c0->cuda(cudaStreamSynchronize(c0->stream), "sync"));
+        HB_TRY(c0->cuda(cudaStreamSynchronize(c0->ea_copy), "sync"));
         c0->last_failed = c0->h_count[0];
         c0->last_replays = c0->h_count[1];
         c0->counters_dirty = (c0->h_count[0] | c0->h_count[1]) != 0;
