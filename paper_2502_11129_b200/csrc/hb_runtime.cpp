@@ -1068,22 +1068,25 @@ std::string batch_failure_text(const uint64_t* seeds, const uint64_t* fail, size
     return msg + ": " + failed.front().second;
 }
 
-// The sequential std::max fold of ea.cpp:101-103 (the first of equal maxima,
-// e.g. +0 before -0; a NaN first element stays) without its one dependent
-// chain: eight independent running maxima, then the first element equal to
-// the maximum.
-double best_fitness(const double* f, size_t n) {
+// The sequential std::max fold of ea.cpp:101-103 starting from `init` (the
+// first of equal maxima, e.g. +0 before -0, wins; a NaN init stays) without
+// its one dependent chain: eight independent running maxima, then the first
+// element equal to the maximum.  Over a final population the parents are
+// sorted descending, so the fold over all of it is the fold over the
+// offspring starting from parent 0.
+double fold_max(double init, const double* f, size_t n) {
     double m[8];
-    for (double& v : m) v = f[0];
+    for (double& v : m) v = init;
     size_t i = 0;
     for (; i + 8 <= n; i += 8)
         for (int k = 0; k < 8; ++k) m[k] = f[i + k] > m[k] ? f[i + k] : m[k];
     for (; i < n; ++i) m[0] = f[i] > m[0] ? f[i] : m[0];
     double mx = m[0];
     for (int k = 1; k < 8; ++k) mx = m[k] > mx ? m[k] : mx;
+    if (init == mx) return init;
     for (size_t j = 0; j < n; ++j)
         if (f[j] == mx) return f[j];
-    return f[0];
+    return init;
 }
 
 // Launch the simulation of n device-resident seeds on c's device; fitness
@@ -1377,7 +1380,7 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
             if (!pg) std::memcpy(genomes_out, c0->h_ea_gen, pop * sizeof(uint64_t));
             if (!pf) std::memcpy(fitness_out, c0->h_ea_fit, pop * sizeof(double));
             if (best_out) {
-                *best_out = best_fitness(fitness_out, pop);
+                *best_out = fold_max(fitness_out[0], fitness_out + mu, mu);
             }
             float ms = 0.f;
             double sel = 0.0;
@@ -1445,7 +1448,7 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     }
     prof.bookkeeping_s += elapsed_s(tb);
     if (best_out) {
-        *best_out = best_fitness(fitness_out, pop);
+        *best_out = fold_max(fitness_out[0], fitness_out + mu, mu);
     }
     prof.total_s = elapsed_s(t_start);
     // the device time of selection+variation is reported as selection (one

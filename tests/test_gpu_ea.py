@@ -19,6 +19,7 @@ def test_native_ea_matches_reference_golden(gpu, golden):
         r = hb.run_ea(g["kind"], g["pop"], g["generations"], g["steps"], gpu, g["seed"])
         assert ["%016x" % int(x) for x in r.population.genomes] == g["genomes"]
         assert [bits(x) for x in r.population.fitnesses] == g["fitness_bits"]
+        assert bits(r.best_fitness) == bits(max(r.population.fitnesses.tolist()))  # ea.cpp:101-103
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
