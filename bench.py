@@ -565,10 +565,11 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
                 "phases_ms_per_run": {k: 1e3 * sum(getattr(p, k + "_s") for p in profs) / a.steps
                                       for k in ("selection", "evaluation", "bookkeeping", "total")},
                 "best_fitness": r.best_fitness, "clocks": clk,
-                # per run: genome init; per evaluation the simulation + fitness
-                # gather; per generation the selection (cluster sort, then tie
-                # fix + select + offspring in one kernel)
-                "gpu_launches": a.steps * (1 + 2 * (G + 1) + 2 * G),
+                # per run: genome init; per evaluation the simulation (+ the
+                # fitness gather, except Box, whose kernel writes fitness);
+                # per generation the selection (cluster sort, then tie fix +
+                # select + offspring in one kernel)
+                "gpu_launches": a.steps * (1 + (1 if int(kind) == 0 else 2) * (G + 1) + 2 * G),
                 "parity": "genomes + fitness bit-identical to reference run_ea"}
         print(json.dumps(line))
     ex.ctx.close()

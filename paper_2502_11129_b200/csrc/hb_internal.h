@@ -36,6 +36,10 @@ struct SimArgs {
     // executed — 16 per variant-step, 10 for steps run at the grounded fixed
     // point (z elided exactly); hb_work_counter reads it
     unsigned long long* ops;
+    // nullable (Box): write each variant's fitness (0 for a failed one) here
+    // instead of the VariantResult records — the generation loop's
+    // evaluation, which needs nothing else
+    double* fitness = nullptr;
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);

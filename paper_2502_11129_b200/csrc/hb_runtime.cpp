@@ -1114,8 +1114,10 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
     }
     hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
                   c->d_out, c->d_fail, c->d_count, nullptr, nullptr, c->d_ops};
+    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO) a.fitness = d_fitness;  // no records, no gather
     HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
-    HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
+    if (!a.fitness)
+        HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
     if (read_counts)
         HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                        c->stream), "D2H count"));
