@@ -18,7 +18,6 @@
 // fitness values agree in their top 32 bits ~2^-20 relative apart).
 #include <atomic>
 #include <cstdlib>
-#include <string>
 
 #include <cooperative_groups.h>
 #include <cub/block/block_radix_rank.cuh>
@@ -99,18 +98,20 @@ unsigned blocks_for(size_t n) { return static_cast<unsigned>((n + 255) / 256); }
 
 // ---------------------------------------------------------------------------
 // One-cluster radix sort of up to 65 536 (high word, index) pairs: the
-// stable 4-pass LSD sort of the selection in a single launch.  CTAS CTAs of
-// 1 024 threads form one cluster (16, non-portable, where the device can
-// schedule it — half the items per SM of the portable 8 and the pass time
-// is issue-bound per SM — else 8); each holds a 1 024 x ITEMS tile in shared
-// memory; per 8-bit digit pass every CTA ranks its tile stably
+// stable LSD sort of the selection in a single launch.  CTAS CTAs of THREADS
+// threads form one cluster (16 x 512 where the device schedules the
+// non-portable cluster, else 8 x 1 024); each holds a THREADS x ITEMS tile in
+// shared memory; per 8-bit digit pass every CTA ranks its tile stably
 // (cub::BlockRadixRankMatch), the CTAs exchange their digit histograms through
 // distributed shared memory, and every item is scattered straight into its
-// destination CTA's next tile (st.shared::cluster).  Sorting ~high word
-// ascending = high word descending; padding (index >= n) gets the largest
-// key and higher indices, so it ends up after every real item.  Replaces the
-// ~20 launches of the device-wide sort (the passes are latency-bound at
-// this size).
+// destination CTA's next tile (st.shared::cluster).  Digits no key varies in
+// are skipped (a non-negative fitness of narrow exponent range: 3 passes).
+// Sorting ~high word ascending = high word descending; padding
+// (index >= n) gets the largest key and higher indices, so it ends up after
+// every real item.  Replaces the ~20 launches of the device-wide sort (the
+// passes are latency-bound at this size).  Measured and dropped: an
+// mbarrier / st.async exchange with no cluster barrier inside the passes
+// (1 us of 26: the passes are bound by the ranking, not the barriers).
 constexpr int kSortMax = 65536;
 template <int THREADS>
 using SortRank = cub::BlockRadixRankMatch<THREADS, 8, false>;  // match.any ranking: small per-warp counters
@@ -118,8 +119,8 @@ using SortRank = cub::BlockRadixRankMatch<THREADS, 8, false>;  // match.any rank
 template <int THREADS, int ITEMS>
 struct SortSmem {
     uint2 buf[THREADS * ITEMS];  // (key, index): every CTA has read its tile into
-                                      // registers before the histogram barrier, so the
-                                      // scatter after it may overwrite the tile in place
+                                 // registers before the histogram barrier, so the
+                                 // scatter after it may overwrite the tile in place
     typename SortRank<THREADS>::TempStorage rank;
     int hist[256];    // this CTA's digit counts (read by the whole cluster)
     int prefix[256];  // this CTA's exclusive digit prefix
@@ -265,221 +266,11 @@ cluster_sort_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* i
     cluster.sync();  // no CTA leaves while another may still read its shared memory
 }
 
-// The same sort without cluster-wide barriers inside the passes: every
-// transfer between CTAs is an st.async into the destination's shared memory
-// that completes bytes on the destination's mbarrier, so each CTA waits only
-// for what it receives.  Per pass (round r, buffers r & 1): every CTA pushes
-// its 256 digit counts to all CTAs (hist_in[r&1][src]), waits for the
-// CTAS x 1 KB it expects, computes its digit offsets, pushes each item to
-// its destination's tile buf[r&1], and waits for its TILE x 8 bytes.
-// Reuse of a buffer two rounds later is ordered by the exchange itself: a
-// CTA pushes round r+2's items only after every CTA's round-r+2 counts
-// arrived, which each CTA sends only after reading its round-r+1 tile (so
-// also its round-r tile and counts).  Round 0 also carries each CTA's key
-// OR / AND (vary_in) for the constant-digit skip.
-template <int THREADS, int ITEMS, int CTAS>
-struct SortSmemA {
-    uint2 buf[2][THREADS * ITEMS];
-    int hist_in[2][CTAS][256];
-    uint4 vary_in[CTAS];
-    typename SortRank<THREADS>::TempStorage rank;
-    int prefix[256];
-    int goff[256];
-    uint32_t wor[32], wand[32];
-    int wsum[8];  // digit-total sums of the scan's 8 warps
-    unsigned long long mbar_hist[2], mbar_tile[2];
-    uint32_t vary;
-};
-
-__device__ __forceinline__ uint32_t mapa(uint32_t local, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-    return r;
-}
-
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    uint32_t done = 0;
-    for (long long spin = 0;; ++spin) {
-        asm volatile("{\n\t.reg .pred p;\n\t"
-                     "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(bar), "r"(parity) : "memory");
-        if (done) return;
-        if (spin > (1ll << 28)) __trap();  // a lost transfer fails the launch instead of hanging
-    }
-}
-
 template <int CTAS, int THREADS>
-__global__ void __launch_bounds__(THREADS, 1)
-cluster_sort_async_kernel(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out, uint64_t* g_dev) {
-    constexpr int ITEMS = kSortMax / (CTAS * THREADS);
-    constexpr int TILE = THREADS * ITEMS;
-    static_assert(THREADS >= 256, "one thread per digit");
-    namespace cg = cooperative_groups;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SortSmemA<THREADS, ITEMS, CTAS>& sm = *reinterpret_cast<SortSmemA<THREADS, ITEMS, CTAS>*>(smem_raw);
-    cg::cluster_group cluster = cg::this_cluster();
-    const int c = static_cast<int>(cluster.block_rank());
-    const int t = threadIdx.x;
-    if (g_dev && c == 0 && t == 0) *g_dev += 1;  // this generation's index (read by tie_select_kernel)
-    const uint32_t bar_h = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.mbar_hist[0]));
-    const uint32_t bar_t = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.mbar_tile[0]));
-    if (t == 0) {
-        for (int b = 0; b < 2; ++b) {
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar_h + 8u * b) : "memory");
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(bar_t + 8u * b) : "memory");
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    const int stripe = (t >> 5) * 32 * ITEMS + (t & 31);
-    uint32_t key[ITEMS], idx[ITEMS];
-    {
-        uint32_t o = 0u, a = 0xffffffffu;
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const int e = c * TILE + stripe + 32 * j;
-            idx[j] = static_cast<uint32_t>(e);
-            key[j] = e < n ? ~static_cast<uint32_t>(__double2hiint(fitness[e])) : 0xffffffffu;
-            if (e < n) {  // padding (all-ones keys, the highest indices) sorts last
-                o |= key[j];  // whatever digits are skipped
-                a &= key[j];
-            }
-        }
-        o = __reduce_or_sync(0xffffffffu, o);
-        a = __reduce_and_sync(0xffffffffu, a);
-        if ((t & 31) == 0) {
-            sm.wor[t >> 5] = o;
-            sm.wand[t >> 5] = a;
-        }
-    }
-    cluster.sync();  // mbarrier inits visible cluster-wide (and wor / wand CTA-wide)
-    const uint32_t buf_sa = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.buf[0][0]));
-    const uint32_t hist_sa = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.hist_in[0][0][0]));
-    const uint32_t vary_sa = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.vary_in[0]));
-    uint32_t use_h = 0u, use_t = 0u;  // bit b: parity of the next wait on buffer b's barrier
-    int round = 0;
-#pragma unroll
-    for (int pass = 0; pass < 4; ++pass) {
-        if (pass > 0 && ((sm.vary >> (8 * pass)) & 0xffu) == 0u) continue;
-        const uint32_t shift = 8u * pass;
-        const int b = round & 1;
-        if (t == 0) {
-            const uint32_t hb = CTAS * 1024u + (round == 0 ? CTAS * 16u : 0u);
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar_h + 8u * b), "r"(hb)
-                         : "memory");
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
-                         :: "r"(bar_t + 8u * b), "r"(static_cast<uint32_t>(TILE * 8)) : "memory");
-        }
-        int ranks[ITEMS];
-        int excl[1];
-        SortRank<THREADS>(sm.rank).RankKeys(key, ranks, DigitAt{shift}, excl);
-        if (t < 256) sm.prefix[t] = excl[0];
-        __syncthreads();
-        // push this CTA's counts of digits 4g..4g+3 to CTA dst, for every (g, dst)
-#pragma unroll
-        for (int w = t; w < 64 * CTAS; w += THREADS) {
-            const int g = w & 63, dst = w >> 6;
-            int cnt[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int d = 4 * g + k;
-                cnt[k] = (d < 255 ? sm.prefix[d + 1] : TILE) - sm.prefix[d];
-            }
-            const uint32_t at = mapa(hist_sa + static_cast<uint32_t>(((b * CTAS + c) * 256 + 4 * g) * 4), dst);
-            const uint32_t bar = mapa(bar_h + 8u * b, dst);
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.s32 [%0], {%1, %2, %3, %4}, [%5];"
-                         :: "r"(at), "r"(cnt[0]), "r"(cnt[1]), "r"(cnt[2]), "r"(cnt[3]), "r"(bar) : "memory");
-        }
-        if (round == 0 && t < 32) {
-            const uint32_t o = __reduce_or_sync(0xffffffffu, t < THREADS / 32 ? sm.wor[t] : 0u);
-            const uint32_t a = __reduce_and_sync(0xffffffffu, t < THREADS / 32 ? sm.wand[t] : 0xffffffffu);
-            if (t < CTAS) {
-                const uint32_t at = mapa(vary_sa + static_cast<uint32_t>(c * 16), t);
-                const uint32_t bar = mapa(bar_h + 8u * b, t);
-                asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];"
-                             :: "r"(at), "r"(o), "r"(a), "r"(0u), "r"(0u), "r"(bar) : "memory");
-            }
-        }
-        mbar_wait(bar_h + 8u * b, (use_h >> b) & 1u);
-        use_h ^= 1u << b;
-        if (round == 0 && t == 0) {
-            uint32_t o = 0u, a = 0xffffffffu;
-#pragma unroll
-            for (int r = 0; r < CTAS; ++r) {
-                o |= sm.vary_in[r].x;
-                a &= sm.vary_in[r].y;
-            }
-            sm.vary = o ^ a;
-        }
-        int tot = 0;
-        if (t < 256) {
-            int before = 0;
-#pragma unroll
-            for (int r = 0; r < CTAS; ++r) {
-                const int v = sm.hist_in[b][r][t];
-                tot += v;
-                before += r < c ? v : 0;
-            }
-            sm.goff[t] = before;
-        }
-        if (t < 256) {  // exclusive scan of the digit totals over 8 warps (+ one warp of warp sums)
-            int incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, incl, o);
-                if ((t & 31) >= o) incl += u;
-            }
-            if ((t & 31) == 31) sm.wsum[t >> 5] = incl;
-            sm.goff[t] += incl - tot;
-        }
-        __syncthreads();
-        if (t < 256) {
-            int run = 0;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) run += w < (t >> 5) ? sm.wsum[w] : 0;
-            sm.goff[t] += run;
-        }
-        __syncthreads();
-        const uint32_t tile_sa = buf_sa + static_cast<uint32_t>(b * TILE * 8);
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint32_t d = (key[j] >> shift) & 0xffu;
-            const int pos = sm.goff[d] + ranks[j] - sm.prefix[d];
-            const uint32_t dst = static_cast<uint32_t>(pos / TILE);
-            const uint32_t at = mapa(tile_sa + static_cast<uint32_t>(pos % TILE) * 8u, dst);
-            const uint32_t bar = mapa(bar_t + 8u * b, dst);
-            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b32 [%0], {%1, %2}, [%3];"
-                         :: "r"(at), "r"(key[j]), "r"(idx[j]), "r"(bar) : "memory");
-        }
-        mbar_wait(bar_t + 8u * b, (use_t >> b) & 1u);
-        use_t ^= 1u << b;
-#pragma unroll
-        for (int j = 0; j < ITEMS; ++j) {
-            const uint2 kv = sm.buf[b][stripe + 32 * j];
-            key[j] = kv.x;
-            idx[j] = kv.y;
-        }
-        ++round;
-    }
-#pragma unroll
-    for (int j = 0; j < ITEMS; ++j) {
-        const int p = c * TILE + stripe + 32 * j;
-        if (p < n) {
-            key_out[p] = ~key[j];
-            idx_out[p] = idx[j];
-        }
-    }
-    cluster.sync();  // no CTA leaves while a peer's transfer into it may be in flight
-}
-
-template <int CTAS, int THREADS, bool ASYNC = false>
 cudaError_t launch_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out, uint64_t* g_dev,
                         cudaStream_t st, bool probe_only = false) {
-    constexpr int ITEMS = kSortMax / (CTAS * THREADS);
-    constexpr size_t smem = ASYNC ? sizeof(SortSmemA<THREADS, ITEMS, CTAS>) : sizeof(SortSmem<THREADS, ITEMS>);
-    void (*kern)(const double*, int, uint32_t*, uint32_t*, uint64_t*);
-    if constexpr (ASYNC) kern = cluster_sort_async_kernel<CTAS, THREADS>;
-    else kern = cluster_sort_kernel<CTAS, THREADS>;
+    constexpr size_t smem = sizeof(SortSmem<THREADS, kSortMax / (CTAS * THREADS)>);
+    auto* kern = cluster_sort_kernel<CTAS, THREADS>;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CTAS);
     cfg.blockDim = dim3(THREADS);
@@ -506,10 +297,11 @@ cudaError_t launch_sort(const double* fitness, int n, uint32_t* key_out, uint32_
 }
 
 // The cluster shape, probed once per device: 16 CTAs of 512 threads
-// (non-portable cluster; half the items per SM of the portable shape, and
-// the pass time is issue-bound per SM) where the device schedules it, else
-// the portable 8 x 1 024.  HB_SORT_SHAPE=8x1024|16x512|16x1024 pins one.
-// State: 0 = unprobed, else shape index + 1.
+// (non-portable cluster: a quarter of the items per SM of the portable
+// 8 x 1 024 and the pass time is issue-bound per SM; measured 26 vs 38 us at
+// 65 536) where the device schedules it, else the portable 8 x 1 024
+// (HB_SORT_CLUSTER8=1 pins it).  State: 0 = unprobed, 1 = 8 x 1 024,
+// 2 = 16 x 512.
 cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out, uint32_t* idx_out,
                                 uint64_t* g_dev, cudaStream_t st) {
     static std::atomic<uint8_t> state[64];
@@ -518,15 +310,10 @@ cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out,
     if (e != cudaSuccess) return e;
     uint8_t s = state[dev & 63].load();
     if (s == 0) {
-        const char* pin = getenv("HB_SORT_SHAPE");
-        const std::string want = pin ? pin : "";
-        if ((want.empty() || want == "16x512") && launch_sort<16, 512>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess)
+        if (!getenv("HB_SORT_CLUSTER8") &&
+            launch_sort<16, 512>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess) {
             s = 2;
-        else if (want == "16x1024" && launch_sort<16, 1024>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess)
-            s = 3;
-        else if (want == "16x512a" && launch_sort<16, 512, true>(nullptr, 0, nullptr, nullptr, nullptr, st, true) == cudaSuccess)
-            s = 4;
-        else {
+        } else {
             cudaGetLastError();  // a refused probe is not an error of this call
             e = launch_sort<8, 1024>(nullptr, 0, nullptr, nullptr, nullptr, st, true);
             if (e != cudaSuccess) return e;
@@ -534,12 +321,8 @@ cudaError_t launch_cluster_sort(const double* fitness, int n, uint32_t* key_out,
         }
         state[dev & 63].store(s);
     }
-    switch (s) {
-        case 2: return launch_sort<16, 512>(fitness, n, key_out, idx_out, g_dev, st);
-        case 3: return launch_sort<16, 1024>(fitness, n, key_out, idx_out, g_dev, st);
-        case 4: return launch_sort<16, 512, true>(fitness, n, key_out, idx_out, g_dev, st);
-        default: return launch_sort<8, 1024>(fitness, n, key_out, idx_out, g_dev, st);
-    }
+    if (s == 2) return launch_sort<16, 512>(fitness, n, key_out, idx_out, g_dev, st);
+    return launch_sort<8, 1024>(fitness, n, key_out, idx_out, g_dev, st);
 }
 
 }  // namespace

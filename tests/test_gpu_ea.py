@@ -169,3 +169,18 @@ def test_select_vary_ties_match_stable_sort(gpu, pop, shape):
     ctr = (np.uint64(g) << np.uint64(32)) + np.arange(pop // 2, dtype=np.uint64)
     assert np.array_equal(nxt[pop // 2:], hb.rng_at(genomes[order] ^ np.uint64(0x243F6A8885A308D3), ctr))
     _ = C
+
+
+def test_select_vary_portable_cluster_shape():
+    """The portable 8 x 1 024 cluster sort (the fallback where a 16-CTA
+    cluster cannot be scheduled; the shape is probed once per process, so the
+    tie tests run again in a child pinned to it)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, HB_SORT_CLUSTER8="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_ea.py"), "-k", "ties_match_stable_sort or golden"],
+                       env=env, cwd=os.path.dirname(here), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
