@@ -1098,15 +1098,19 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
     const bool dev_init = init_on_device(c, kind);
     HB_TRY(ensure_capacity(c, kind, n, !dev_init));
     if (!dev_init) {
+        Trace tr("eval-init");
         HB_TRY(c->cuda(cudaMemcpyAsync(c->h_seeds, d_seeds, n * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                        c->stream), "D2H seeds"));
         HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "stream sync"));
+        tr.mark("d2h_seeds+wait");
         double* soa = c->h_init;
         const uint64_t* hs = c->h_seeds;
         pool_of(c).run(n, [&](size_t b, size_t e) { build_range(kind, hs, b, e, soa, n); }, 64);
+        tr.mark("build");
         const size_t rows = static_cast<size_t>(hb::state_rows(kind));
         HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
                                        cudaMemcpyHostToDevice, c->stream), "H2D init"));
+        tr.mark("h2d_enqueue");
     }
     if (c->counters_dirty) {
         HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
