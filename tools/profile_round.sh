@@ -7,6 +7,7 @@
 #   launches_box.csv        ncu launch list of the default bench command
 #   prof_box.ncu-rep        ncu --set full capture of one box_kernel launch
 #   bench_ea_*.json         configs[4] generation loop (box, box_and_ball) + reference arms
+#   launches_ea_box.csv     ncu launch list of one box generation loop (sort / select / eval kernels)
 #   sweeps.json             variant / step sweeps (tools/sweep.py)
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/bench_box.json 2> gpurun_out/bench_box.err
@@ -26,5 +27,8 @@ for m in box box_and_ball; do
   timeout 600 python bench.py --workload ea --model $m > gpurun_out/bench_ea_$m.json 2> /dev/null
   timeout 600 python bench.py --workload ea --model $m --impl reference > gpurun_out/bench_ea_${m}_ref.json 2> /dev/null
 done
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  --log-file gpurun_out/launches_ea_box.csv python bench.py --workload ea --model box --steps 1 --warmup 3 \
+  > /dev/null 2>&1
 timeout 1800 python tools/sweep.py --out gpurun_out/sweeps.json > gpurun_out/sweep.log 2>&1
 ls -la gpurun_out
