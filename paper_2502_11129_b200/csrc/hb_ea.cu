@@ -47,6 +47,43 @@ __global__ void key_hi_kernel(const double* fitness, size_t n, uint32_t* key, ui
     idx[i] = static_cast<uint32_t>(i);
 }
 
+// Position order of two members of one run of equal high words: low word
+// descending, then index ascending (a total order, so an unstable sort of
+// the run gives exactly the stable sort's result).
+__device__ __forceinline__ bool run_before(uint32_t ia, uint32_t ib, const double* fitness) {
+    const uint32_t la = static_cast<uint32_t>(__double2loint(fitness[ia]));
+    const uint32_t lb = static_cast<uint32_t>(__double2loint(fitness[ib]));
+    return la > lb || (la == lb && ia < ib);
+}
+
+// Runs are a few elements, sorted by insertion; a long run (only crafted
+// fitness has thousands of values sharing their top 32 bits) is heap-sorted
+// instead, O(L log L) rather than O(L^2) on its one thread.
+constexpr size_t kInsertionMax = 32;
+
+__device__ void heap_sift(uint32_t* a, size_t i, size_t len, const double* fitness) {
+    const uint32_t x = a[i];
+    for (;;) {
+        size_t c = 2 * i + 1;
+        if (c >= len) break;
+        if (c + 1 < len && run_before(a[c], a[c + 1], fitness)) ++c;  // the later-placed child
+        if (!run_before(x, a[c], fitness)) break;
+        a[i] = a[c];
+        i = c;
+    }
+    a[i] = x;
+}
+
+__device__ void heap_sort_run(uint32_t* a, size_t len, const double* fitness) {
+    for (size_t i = len / 2; i-- > 0;) heap_sift(a, i, len, fitness);
+    for (size_t k = len; k-- > 1;) {
+        const uint32_t t = a[0];
+        a[0] = a[k];
+        a[k] = t;
+        heap_sift(a, 0, k, fitness);
+    }
+}
+
 // Tie fix, selection and variation in one pass over the sorted order
 // (ea.cpp:60-79).  The sort ordered (high word desc, index asc); within a run
 // of equal high words the order must be low word descending, index
@@ -65,7 +102,9 @@ __global__ void tie_select_kernel(const uint64_t* genomes, const double* fitness
     if (p > 0 && key[p - 1] == kp) return;  // inside a run: its first position emits it
     size_t end = p + 1;
     while (end < n && key[end] == kp) ++end;
-    for (size_t a = p + 1; a < end; ++a) {
+    if (end - p > kInsertionMax)
+        heap_sort_run(order + p, end - p, fitness);  // bounded cost for crafted long runs
+    for (size_t a = p + 1; a < end && end - p <= kInsertionMax; ++a) {
         const uint32_t ia = order[a];
         const uint32_t la = static_cast<uint32_t>(__double2loint(fitness[ia]));
         size_t b = a;

@@ -119,7 +119,8 @@ def test_device_sharded_ea_equals_reference_loop(world):
 
 
 @pytest.mark.parametrize("pop,shape", [(4096, "mixed"), (40002, "mixed"), (65536, "mixed"), (70000, "mixed"),
-                                       (4096, "sparse"), (40002, "sparse"), (65536, "sparse")])
+                                       (4096, "sparse"), (40002, "sparse"), (65536, "sparse"),
+                                       (4096, "onerun"), (40002, "onerun")])
 def test_select_vary_ties_match_stable_sort(gpu, pop, shape):
     """hb_ea_select_vary on crafted fitness: exact duplicates, +0, long runs of
     equal high words with different low words — parents and their order must
@@ -127,7 +128,8 @@ def test_select_vary_ties_match_stable_sort(gpu, pop, shape):
     Populations below / at the cluster sort's 65 536 (partial and full tiles)
     and above it (the device-wide sort).  "sparse": high words whose top byte
     and bits 8-15 are shared by every key, so the cluster sort skips those
-    digit passes (and bits 0-7 / 16-23 still order them)."""
+    digit passes (and bits 0-7 / 16-23 still order them).  "onerun": one run
+    of equal high words over the whole population (the heap-sorted path)."""
     import ctypes as C
 
     import torch
@@ -146,6 +148,8 @@ def test_select_vary_ties_match_stable_sort(gpu, pop, shape):
               | rng.integers(0, 256, pop, dtype=np.uint64))
         hi[sel] = hi[grp[sel]]  # runs of shared high words
         fit = ((hi << np.uint64(32)) | (bits & np.uint64(0xFFFFFFFF))).view(np.float64).copy()
+    elif shape == "onerun":  # every key shares one high word: a single run, heap-sorted
+        fit = ((np.uint64(0x3FE23456) << np.uint64(32)) | (bits & np.uint64(0xFFFFFFFF))).view(np.float64).copy()
     else:
         fit[:7] = 0.0                                                      # +0 fitness
     fit[rng.choice(pop, 300, replace=False)] = fit[rng.choice(pop, 300)]  # exact duplicates
