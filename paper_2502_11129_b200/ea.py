@@ -18,8 +18,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import lib
-from .executor import (BatchExecutor, BatchFailure, BatchRequest, GpuExecutor, ModelKind,
-                       MultiGpuExecutor)
+from .executor import BatchExecutor, BatchRequest, GpuExecutor, ModelKind, MultiGpuExecutor
 
 K_INIT_KEY = 0x8F5D4C3B2A190807
 K_CHILD_KEY = 0x243F6A8885A308D3

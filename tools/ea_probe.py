@@ -2,7 +2,6 @@
 import sys
 import time
 
-import numpy as np
 
 sys.path.insert(0, ".")
 import paper_2502_11129_b200 as hb  # noqa: E402
