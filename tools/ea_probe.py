@@ -2,7 +2,6 @@
 import sys
 import time
 
-
 sys.path.insert(0, ".")
 import paper_2502_11129_b200 as hb  # noqa: E402
 from paper_2502_11129_b200.ea import run_ea_native  # noqa: E402
