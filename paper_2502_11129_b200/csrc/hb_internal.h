@@ -43,6 +43,11 @@ struct SimArgs {
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);
+// Initial SoA state rows (state_rows(kind) x n, row stride n) of a
+// multi-body kind from the seeds and the host's cos / sin rows
+// (2 init_angles(kind) x n): hb_init.cu.
+cudaError_t launch_init(int kind, const uint64_t* seeds, const double* trig, size_t n, double* soa,
+                        cudaStream_t st);
 // The Box stepping launch through a per-context one-node CUDA graph whose
 // kernel parameters are updated in place each call: cheaper on the host and
 // on the device than a plain launch (the drop-in call's fixed cost).

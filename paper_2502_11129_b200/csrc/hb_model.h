@@ -45,6 +45,11 @@ HB_HD constexpr int constraints(int k) {
 // CPG rows of kind 4: x[4], y[4], omega[4], coupling[4].
 HB_HD constexpr int cpg_rows(int k) { return k == 4 ? 16 : 0; }
 HB_HD constexpr int state_rows(int k) { return 6 * bodies(k) + constraints(k) + cpg_rows(k); }
+// Distinct body angles build_model takes cos / sin of (simkernel.cpp:77-84:
+// heading + 0.15 j per body, the humanoid's two rails share j = b % 16;
+// kind 4: heading + pi/2 l per limb).  The product computes these with the
+// host's libm and the rest of the initial state on the device.
+HB_HD constexpr int init_angles(int k) { return k == 1 ? 2 : k == 2 ? 12 : k == 3 ? 16 : k == 4 ? 4 : 0; }
 
 // Constraint c of model k: endpoints (a, b) and whether it is a soft link.
 // Kind 4: c = 2l core-hinge (0, 1+2l), c = 2l+1 hinge-tip (1+2l, 2+2l),

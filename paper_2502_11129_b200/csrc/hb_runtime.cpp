@@ -63,12 +63,14 @@ public:
     }
     int size() const { return n_; }
 
-    // fn(begin, end) over [0, total) in up to `n_` contiguous chunks of at
-    // least `grain` items.
+    // fn(begin, end) over [0, total) in contiguous chunks of at least `grain`
+    // items, up to 8 per thread, taken dynamically: threads that wake late
+    // (a futex wake-up after the spin window is tens of µs) find the chunks
+    // already done by the caller and the early ones.
     void run(size_t total, const std::function<void(size_t, size_t)>& fn, size_t grain = 1) {
         if (total == 0) return;
         const size_t max_parts = std::max<size_t>(1, total / std::max<size_t>(1, grain));
-        const int parts = static_cast<int>(std::min<size_t>(n_, max_parts));
+        const int parts = n_ == 1 ? 1 : static_cast<int>(std::min<size_t>(8 * static_cast<size_t>(n_), max_parts));
         if (parts == 1) {
             fn(0, total);
             return;
@@ -247,6 +249,23 @@ void build_range(int kind, const uint64_t* seeds, size_t b, size_t e, double* so
     }
 }
 
+// cos / sin of build_model's body angles (init_angles(kind) of them; the
+// host libm's values, exactly as build_one / build_cpg take them) for the
+// device initialiser: cos of angle j at row j, sin at row J + j.
+void trig_range(int kind, const uint64_t* seeds, size_t b, size_t e, double* trig, size_t ld) {
+    const int J = hb::init_angles(kind);
+    const double step = kind == hb::CpgHinge ? 1.5707963267948966 : 0.15;
+    for (size_t i = b; i < e; ++i) {
+        Stream rs{seeds[i], 3};  // draw 3 = heading (after drop height, lx, ly)
+        const double heading = rs.range(0.0, 2.0 * 3.14159265358979323846);
+        for (int j = 0; j < J; ++j) {
+            const double a = heading + step * static_cast<double>(j);
+            trig[j * ld + i] = std::cos(a);
+            trig[(J + j) * ld + i] = std::sin(a);
+        }
+    }
+}
+
 inline long long __double_as_longlong_host(double x) {
     long long v;
     std::memcpy(&v, &x, sizeof v);
@@ -274,6 +293,8 @@ struct hb_ctx {
     // device buffers
     double* d_init = nullptr;
     size_t d_init_cap = 0;  // doubles
+    double* d_trig = nullptr;  // host-computed cos / sin rows for the device initialiser
+    size_t d_trig_cap = 0;     // doubles
     uint64_t* d_seeds = nullptr;
     hb_variant_result* d_out = nullptr;  // 32-byte results per variant
     uint64_t* d_fail = nullptr;
@@ -358,6 +379,8 @@ hb_status ensure_capacity(hb_ctx* c, int kind, size_t n, bool need_init) {
     if (need_init) {
         const size_t need = static_cast<size_t>(hb::state_rows(kind)) * n;
         HB_TRY(grow_dev(c, &c->d_init, c->d_init_cap, need, "cudaMalloc(init)"));
+        const size_t trig = 2 * static_cast<size_t>(hb::init_angles(kind)) * n;
+        if (trig) HB_TRY(grow_dev(c, &c->d_trig, c->d_trig_cap, trig, "cudaMalloc(trig)"));
         if (need > c->h_init_cap) {
             if (c->h_init) cudaFreeHost(c->h_init);
             c->h_init = nullptr;
@@ -411,6 +434,13 @@ bool fp32_for(const hb_ctx* c, int kind) { return c->precision == HB_PRECISION_F
 
 bool init_on_device(const hb_ctx* c, int kind) {
     return kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO;
+}
+
+// Multi-body kinds on the product kernels: the host computes only the libm
+// cos / sin rows, the device builds the state (hb_init.cu).  The generic
+// kernel variant keeps the all-host build_model (an independent path).
+bool trig_init(const hb_ctx* c, int kind) {
+    return kind != hb::Box && c->kernel_variant == HB_KERNEL_AUTO;
 }
 
 constexpr size_t kParallelCopyMin = 2048;  // min items per host thread for copies / assembly
@@ -476,6 +506,15 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
             pool_of(c).run(n, [&](size_t b, size_t e) {
                 std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
             }, kParallelCopyMin);
+    } else if (trig_init(c, kind)) {
+        double* trig = c->h_init;
+        pool_of(c).run(n, [&](size_t b, size_t e) {
+            if (!direct) std::memcpy(hs + b, seeds + b, (e - b) * sizeof(uint64_t));
+            trig_range(kind, seeds, b, e, trig, n);
+        }, 64);
+        const size_t rows = 2 * static_cast<size_t>(hb::init_angles(kind));
+        HB_TRY(c->cuda(cudaMemcpyAsync(c->d_trig, c->h_init, rows * n * sizeof(double),
+                                       cudaMemcpyHostToDevice, c->stream), "H2D trig"));
     } else {
         double* soa = c->h_init;
         pool_of(c).run(n, [&](size_t b, size_t e) {
@@ -489,6 +528,8 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
     tr.mark(direct ? "host(direct)" : "host(staged)");
     HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, direct ? seeds : c->h_seeds, n * sizeof(uint64_t),
                                    cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+    if (!dev_init && trig_init(c, kind))
+        HB_TRY(c->cuda(hb::launch_init(kind, c->d_seeds, c->d_trig, n, c->d_init, c->stream), "init kernel"));
     tr.mark("h2d_enqueue");
     c->staged_kind = kind;
     c->staged_n = n;
@@ -626,7 +667,7 @@ void hb_ctx_destroy(hb_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_init); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
+    cudaFree(c->d_init); cudaFree(c->d_trig); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
     cudaFree(c->d_final); cudaFree(c->d_scratch); cudaFree(c->d_count); cudaFree(c->d_ea_fit);
     cudaFree(c->d_ops);
     hb::destroy_box_graph(c->box_graph);
@@ -1105,11 +1146,20 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
         tr.mark("d2h_seeds+wait");
         double* soa = c->h_init;
         const uint64_t* hs = c->h_seeds;
-        pool_of(c).run(n, [&](size_t b, size_t e) { build_range(kind, hs, b, e, soa, n); }, 64);
-        tr.mark("build");
-        const size_t rows = static_cast<size_t>(hb::state_rows(kind));
-        HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
-                                       cudaMemcpyHostToDevice, c->stream), "H2D init"));
+        if (trig_init(c, kind)) {
+            pool_of(c).run(n, [&](size_t b, size_t e) { trig_range(kind, hs, b, e, soa, n); }, 64);
+            tr.mark("trig");
+            const size_t rows = 2 * static_cast<size_t>(hb::init_angles(kind));
+            HB_TRY(c->cuda(cudaMemcpyAsync(c->d_trig, c->h_init, rows * n * sizeof(double),
+                                           cudaMemcpyHostToDevice, c->stream), "H2D trig"));
+            HB_TRY(c->cuda(hb::launch_init(kind, d_seeds, c->d_trig, n, c->d_init, c->stream), "init kernel"));
+        } else {
+            pool_of(c).run(n, [&](size_t b, size_t e) { build_range(kind, hs, b, e, soa, n); }, 64);
+            tr.mark("build");
+            const size_t rows = static_cast<size_t>(hb::state_rows(kind));
+            HB_TRY(c->cuda(cudaMemcpyAsync(c->d_init, c->h_init, rows * n * sizeof(double),
+                                           cudaMemcpyHostToDevice, c->stream), "H2D init"));
+        }
         tr.mark("h2d_enqueue");
     }
     if (c->counters_dirty) {
