@@ -207,11 +207,14 @@ def gpu_generic():
 
 
 @pytest.mark.parametrize("kind,n,steps", [(0, 200000, 300), (1, 65536, 200), (2, 16384, 100),
-                                          (3, 8192, 40)])
+                                          (3, 8192, 40), (4, 16384, 100), (1, 3000, 1), (3, 1000, 1)])
 def test_optimised_equals_generic_kernel(gpu, gpu_generic, kind, n, steps):
-    """The optimised kernels (device-side Box init, branch-free projection with
-    exact replay, two-lane humanoid) against the plain reference-order kernel
-    (host init, library sqrt / '/') on large random batches, bit for bit."""
+    """The optimised kernels (device-side initial states — Box from the seed
+    alone, the multi-body kinds from host cos / sin rows —, branch-free
+    projection with exact replay, two-lane humanoid) against the plain
+    reference-order kernel (all-host build_model, library sqrt / '/') on
+    large random batches, bit for bit (1-step cases: the initial state
+    itself up to one step)."""
     rng = np.random.default_rng(7 + kind)
     seeds = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
     a = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
