@@ -91,8 +91,11 @@ const char* hb_last_error(const hb_ctx* ctx);
 int hb_ctx_device(const hb_ctx* ctx);
 /* The cudaStream_t every launch of this context is issued on. */
 void* hb_ctx_stream(hb_ctx* ctx);
-/* Host threads used by the host-side initialiser (default: all hardware
- * threads, capped at 64). 0 = default. */
+/* Host threads used for the host side of initialisation — the libm
+ * cos / sin of build_model's body angles (the rest of the multi-body state
+ * is built on the device; the generic kernel variant builds all of it on
+ * the host) — and for staging copies (default: all hardware threads,
+ * capped at 64). 0 = default. */
 hb_status hb_ctx_set_host_threads(hb_ctx* ctx, int threads);
 
 /* Kernel family used by this context.  HB_KERNEL_AUTO (default) = the
@@ -110,7 +113,7 @@ hb_status hb_ctx_set_kernel(hb_ctx* ctx, int variant);
  * mode of SURVEY.md §8 row f3 for the multi-body models: float-float
  * positions, FP32 increments, FMA-compensated constants, MUFU rsqrt; NOT
  * bit-exact — fitness within the tolerance stated in tests/test_gpu_fp32.py,
- * checksums of this mode's own state; host-built initial states.  Box keeps
+ * checksums of this mode's own state; the same initial states.  Box keeps
  * the (faster) bit-exact FP64 kernel in either mode. */
 #define HB_PRECISION_FP64 0
 #define HB_PRECISION_FP32 1
@@ -224,8 +227,11 @@ hb_status hb_fp64_peak(hb_ctx* ctx, double* ops_per_s, double* ms);
  * run_ea with every generation's evaluation, selection (stable descending
  * sort of fitness) and variation on the devices; only the per-generation
  * fitness of each device's offspring slice crosses to device 0 (peer copy
- * over NVLink) and, for models initialised on the host, the offspring seeds
- * go through the host initialiser.  Offspring are sharded over the
+ * over NVLink) and, for the multi-body models, the offspring seeds go to the
+ * host for the libm cos / sin rows of their initial states.  With one
+ * context and Box the whole loop is queued without a host round trip per
+ * generation (one failure check at the end; a blow-up re-runs the loop with
+ * a check per generation to report it).  Offspring are sharded over the
  * `count` contexts by hb_plan_allocation_n(device_times) (NULL = equal).
  * Outputs (host): final population genomes / fitness (pop each, parents ++
  * offspring), best fitness, phase profile; history_* (nullable) receive the
