@@ -52,6 +52,20 @@ def test_config5_population_box_and_ball():
     assert r.profile.evaluation_s > 0
 
 
+@pytest.mark.parametrize("pop", [65536, 70000])
+def test_queued_box_loop_both_sorts(gpu, pop):
+    """The queued one-device Box loop (no host round trip per generation)
+    through the cluster sort (<= 65 536) and the device-wide sort (above),
+    each generation's counter advanced on the device, against the oracle's
+    run_ea; then the same context again (persistent buffers, graphs reused)."""
+    g, f = O.run_ea(0, pop, 3, 50, seed=4)
+    for _ in range(2):
+        r = hb.run_ea(0, pop, 3, 50, gpu, seed=4)
+        assert np.array_equal(r.population.genomes, g)
+        assert np.array_equal(r.population.fitnesses, f)
+        assert r.best_fitness == max(f.tolist())
+
+
 def test_sharded_over_two_contexts(gpu):
     """Two contexts on the same device stand in for two GPUs: offspring are
     split by the N-way splitter and fitness gathered by peer copy."""
