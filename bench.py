@@ -277,13 +277,23 @@ def run_reference(a, ws, rank):
 
 
 def latency_bound(a, n, ops_exec, kernel_ms, clk):
-    """Dependent-chain latency roofline of the Box kernel."""
+    """Dependent-chain latency roofline of the Box kernel and
+    of the CpgHinge kernel (64 serial projections per step)."""
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    if a.model == "cpg_hinge":
+        # 8 sweeps x 8 serial slots (every link of the core body is serial),
+        # each projection a ~166-cycle dependent chain: 3 DADD (d), 3 DMUL +
+        # 2 DADD (d^2), MUFU + 7 FP64 (sqrt), 5 (certified division), 2 (apply)
+        cycles = 64 * 166.0 * a.sim_steps
+        t_ideal_ms = cycles / (mhz * 1e6) * 1e3
+        return {"chain_cycles_per_variant": cycles, "ideal_ms": t_ideal_ms, "frac": t_ideal_ms / kernel_ms,
+                "model": "64 serial projections per step x ~166 cycles (binding while <= 1 warp per SMSP, "
+                         "n <= 18 944)"}
     if a.model != "box" or ops_exec is None:
         return None
     steps = a.sim_steps
     gnd = max(0.0, (16.0 * n * steps - ops_exec) / (6.0 * n))  # average grounded steps per variant
     cycles = 8.07 * (5.0 * gnd + 6.0 * (steps - gnd))
-    mhz = (clk or {}).get("sm_mhz") or 1965.0
     t_ideal_ms = cycles / (mhz * 1e6) * 1e3
     return {"chain_cycles_per_variant": cycles, "grounded_steps_per_variant": gnd,
             "ideal_ms": t_ideal_ms, "frac": t_ideal_ms / kernel_ms,
