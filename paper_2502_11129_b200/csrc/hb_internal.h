@@ -49,12 +49,14 @@ cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int
 cudaError_t launch_init(int kind, const uint64_t* seeds, const double* trig, size_t n, double* soa,
                         cudaStream_t st);
 // The Box stepping launch through a per-context one-node CUDA graph whose
-// kernel parameters are updated in place each call: cheaper on the host and
-// on the device than a plain launch (the drop-in call's fixed cost).
+// kernel parameters are updated in place when they change: cheaper on the
+// host and on the device than a plain launch (the drop-in call's fixed cost).
 struct BoxGraph {
     cudaGraph_t graph[2] = {nullptr, nullptr};  // [from seeds, from states]
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
     cudaGraphNode_t node[2] = {nullptr, nullptr};
+    SimArgs last[2];              // the parameters the instantiated node holds
+    unsigned last_block[2] = {0, 0};
 };
 cudaError_t launch_box_graph(BoxGraph& g, const SimArgs& a, cudaStream_t st, int sms);
 void destroy_box_graph(BoxGraph& g);
@@ -67,7 +69,8 @@ cudaError_t launch_fastpath_check(const double* x, const double* y, size_t n, do
                                   double* o2, double* o3, unsigned char* flags, cudaStream_t st);
 
 // Generation loop helpers (hb_ea.cu).
-// g_dev (optional): the graph-replayed loop's generation counter, set to 1
+// g_dev (optional): the graph-replayed loop's generation counter, reset to 0
+// (each selection graph's first kernel advances it)
 cudaError_t ea_init_genomes(uint64_t seed, size_t pop, uint64_t* d_genomes, cudaStream_t st,
                             uint64_t* g_dev = nullptr);
 cudaError_t ea_fitness_from_results(const hb_variant_result* out, size_t n, double* fitness,
