@@ -66,6 +66,18 @@ def test_queued_box_loop_both_sorts(gpu, pop):
         assert r.best_fitness == max(f.tolist())
 
 
+@pytest.mark.parametrize("kind,pop", [(4, 1024), (2, 3000), (3, 512)])
+def test_native_ea_vs_oracle_other_models(gpu, kind, pop):
+    """The generation loop for CpgHinge (parity against its defining oracle,
+    kind 4 has no reference model), the arm and the humanoid: final
+    population and best fitness bit-identical to the oracle's run_ea."""
+    g, f = O.run_ea(kind, pop, 3, 40, seed=3)
+    r = hb.run_ea(kind, pop, 3, 40, gpu, seed=3)
+    assert np.array_equal(r.population.genomes, g)
+    assert np.array_equal(r.population.fitnesses.view(np.uint64), f.view(np.uint64))
+    assert r.best_fitness == max(f.tolist())
+
+
 def test_sharded_over_two_contexts(gpu):
     """Two contexts on the same device stand in for two GPUs: offspring are
     split by the N-way splitter and fitness gathered by peer copy."""
