@@ -52,7 +52,7 @@ def test_config5_population_box_and_ball():
     assert r.profile.evaluation_s > 0
 
 
-@pytest.mark.parametrize("pop", [65536, 70000])
+@pytest.mark.parametrize("pop", [2, 4, 66, 65536, 70000])
 def test_queued_box_loop_both_sorts(gpu, pop):
     """The queued one-device Box loop (no host round trip per generation)
     through the cluster sort (<= 65 536) and the device-wide sort (above),
@@ -66,7 +66,7 @@ def test_queued_box_loop_both_sorts(gpu, pop):
         assert r.best_fitness == max(f.tolist())
 
 
-@pytest.mark.parametrize("kind,pop", [(4, 1024), (2, 3000), (3, 512)])
+@pytest.mark.parametrize("kind,pop", [(4, 1024), (2, 3000), (3, 512), (1, 2), (4, 6)])
 def test_native_ea_vs_oracle_other_models(gpu, kind, pop):
     """The generation loop for CpgHinge (parity against its defining oracle,
     kind 4 has no reference model), the arm and the humanoid: final
