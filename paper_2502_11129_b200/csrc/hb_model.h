@@ -92,7 +92,7 @@ constexpr uint64_t kChildKey = 0x243F6A8885A308D3ull;
 constexpr uint64_t kFnvOffset = 0xcbf29ce484222325ull;
 constexpr uint64_t kFnvPrime = 0x100000001b3ull;
 HB_HD uint64_t fnv_absorb_bits(uint64_t h, uint64_t bits) {
-#if defined(__CUDACC__)
+#if defined(__CUDA_ARCH__)
 #pragma unroll
 #endif
     for (int i = 0; i < 8; ++i) {
