@@ -78,6 +78,20 @@ def test_native_ea_vs_oracle_other_models(gpu, kind, pop):
     assert r.best_fitness == max(f.tolist())
 
 
+@pytest.mark.parametrize("kind", [0, 1])
+def test_config5_full_vs_reference_run_ea(gpu, kind):
+    """BASELINE configs[4] at full size (65 536 genomes x 5 generations x
+    1 000 steps) against the reference's own run_ea (oracle/_ref, all host
+    threads): final genomes, fitness and best fitness bit for bit."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    g, f = O.ref_run_ea(kind, 65536, 5, 1000, seed=0)
+    r = hb.run_ea(kind, 65536, 5, 1000, gpu, seed=0)
+    assert np.array_equal(r.population.genomes, g)
+    assert np.array_equal(r.population.fitnesses.view(np.uint64), f.view(np.uint64))
+    assert bits(r.best_fitness) == bits(max(f.tolist()))
+
+
 def test_sharded_over_two_contexts(gpu):
     """Two contexts on the same device stand in for two GPUs: offspring are
     split by the N-way splitter and fitness gathered by peer copy."""

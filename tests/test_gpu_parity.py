@@ -305,6 +305,25 @@ def test_baseline_sizes_subsampled_vs_oracle(gpu, kind, n, steps, stride):
     assert cc == np.bitwise_xor.reduce(again["checksum"] * np.uint64(0x9E3779B97F4A7C15))
 
 
+@pytest.mark.parametrize("kind,n,steps", [
+    (0, 16384, 1000),   # configs[1], the headline, every variant
+    (1, 8192, 5000),    # configs[2] size, box_and_ball
+    (2, 8192, 1000),
+    (3, 8192, 1000),
+])
+def test_full_batches_vs_reference_library(gpu, kind, n, steps):
+    """Every record of a full BASELINE-size batch against the reference's own
+    cpu_executor (oracle/_ref: the reference sources compiled in place,
+    all host threads), bit for bit."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    seeds = np.arange(n, dtype=np.uint64)
+    got = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
+    rc, want, _, _, msg = O.ref_cpu_run(kind, seeds, steps, 0)
+    assert rc == 0, msg
+    assert np.array_equal(got, want)
+
+
 def test_nvml_utilisation_trace():
     """GpuExecutor(monitor=True) fills BatchResult.utilization_trace from NVML
     (the accelerator side the reference leaves at 0, monitor.cpp:164)."""
