@@ -307,6 +307,7 @@ def test_baseline_sizes_subsampled_vs_oracle(gpu, kind, n, steps, stride):
 
 @pytest.mark.parametrize("kind,n,steps", [
     (0, 16384, 1000),   # configs[1], the headline, every variant
+    (0, 32768, 20000),  # configs[3] endpoint
     (1, 8192, 5000),    # configs[2] size, box_and_ball
     (2, 8192, 1000),
     (3, 8192, 1000),
