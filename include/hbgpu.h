@@ -34,12 +34,17 @@ extern "C" {
 
 #define HBGPU_ABI_VERSION 1
 
-/* hetbench::ModelKind (include/hetbench/simkernel.hpp:14) — same ordinals. */
+/* hetbench::ModelKind (include/hetbench/simkernel.hpp:14) — same ordinals.
+ * HB_CPG_HINGE (4) is NOT a reference model: the "Revolve2-style modular
+ * robot with hinge joints + CPG controller" of BASELINE configs[2] (SPEC.md:101
+ * leaves it undefined); its definition and only oracle is oracle/hb_oracle.c
+ * (hbo_cpg_*).  Every entry point taking a `kind` accepts 0..4. */
 typedef enum {
     HB_BOX = 0,
     HB_BOX_AND_BALL = 1,
     HB_ARM_WITH_ROPE = 2,
-    HB_HUMANOID = 3
+    HB_HUMANOID = 3,
+    HB_CPG_HINGE = 4
 } hb_model_kind;
 
 typedef enum {
@@ -124,6 +129,21 @@ hb_status hb_ctx_set_precision(hb_ctx* ctx, int precision);
  * and writes the results through the host mapping — no H2D / D2H operation
  * on the call's critical path.  0 disables it (always stage + DMA). */
 hb_status hb_ctx_set_zero_copy(hb_ctx* ctx, int enable);
+
+/* Fault injection (test seam; the counterpart of the reference's
+ * simulate_fn seam, executor.hpp:89-90, that its tests use to make a back-end
+ * throw).  Applies to hb_run_batch calls on this context until reset:
+ *   HB_FAULT_NONE    no injection (default);
+ *   HB_FAULT_BLOWUP  every variant whose seed == `seed` is reported as blown
+ *                    up at step 1 (fail_step 1, record {seed, 0, 0, 1},
+ *                    HB_BLOWUP_PARTIAL) — the batch_failure path;
+ *   HB_FAULT_DEVICE  every call fails with HB_CUDA_ERROR, as a dead device —
+ *                    the path on which calibrate / run_hybrid treat a
+ *                    back-end as failed (scheduler.cpp:40-49,162-183). */
+#define HB_FAULT_NONE 0
+#define HB_FAULT_BLOWUP 1
+#define HB_FAULT_DEVICE 2
+hb_status hb_ctx_inject_fault(hb_ctx* ctx, int mode, uint64_t seed);
 
 /* Page-locked host memory (cudaHostAlloc, portable + mapped).  hb_run_batch / hb_fetch
  * DMA the results straight into an `out` buffer allocated here (no staging

@@ -110,6 +110,53 @@ int main() {
               "run_ea_humanoid_identical");
         std::printf("  run_ea over gpu_executor: evaluation_fraction=%.3f\n", b.profile.evaluation_fraction());
     }
+    // batch_failure mapping (executor.cpp:20-28,121-128): a variant reported
+    // as blown up by the backend (hb_ctx_inject_fault, the test seam standing
+    // in for a crafted state) surfaces as the reference's batch_failure with
+    // the numerical_blowup text, and the rest of the batch completes.
+    {
+        std::vector<std::uint64_t> seeds(4096);
+        std::iota(seeds.begin(), seeds.end(), std::uint64_t{0});
+        const std::uint64_t bad = 3001;
+        BatchRequest r{ModelKind::BoxAndBall, seeds, 300};
+        const BatchResult want = cpu.run(r);
+        hb_ctx_inject_fault(gpu.context(), HB_FAULT_BLOWUP, bad);
+        bool ok = false;
+        std::string detail = "no batch_failure";
+        try {
+            gpu.run(r);
+        } catch (const batch_failure& e) {
+            std::vector<VariantResult> rest;
+            for (const VariantResult& v : want.results)
+                if (v.seed != bad) rest.push_back(v);
+            const std::string msg = "coordinate left the stable regime at t=0.002000 (seed 3001)";
+            ok = e.failed().size() == 1 && e.failed()[0].first == bad && e.failed()[0].second == msg &&
+                 e.completed() == rest &&
+                 std::string(e.what()) == "batch failed for seed 3001: " + msg;
+            detail = e.what();
+        }
+        check(ok, "batch_failure_mapping", detail);
+
+        // run_hybrid (scheduler.cpp:162-183): the accelerator share throws
+        // batch_failure, is re-dispatched to the CPU, the result is degraded
+        // and the merge is the all-CPU result.
+        const AllocationPlan plan = plan_allocation(CalibrationProfile{ModelKind::BoxAndBall, 300, 64, 1.0, 0.01,
+                                                                       0.01, true, true},
+                                                    seeds.size());
+        const HybridResult hr = run_hybrid(plan, r, cpu, gpu, 0.0, ExecMode::Emulated);
+        check(hr.degraded && hr.merged == want.results && plan.n_accel > 0, "run_hybrid_redispatch_on_blowup");
+
+        // a dead device (HB_FAULT_DEVICE -> std::runtime_error): calibrate
+        // flags the accelerator failed and the plan gives it nothing
+        // (scheduler.cpp:40-49,70-72)
+        hb_ctx_inject_fault(gpu.context(), HB_FAULT_DEVICE, 0);
+        const CalibrationProfile p = calibrate(ModelKind::BoxAndBall, 300, 256, cpu, gpu);
+        const AllocationPlan dead = plan_allocation(p, seeds.size());
+        check(p.cpu_ok && !p.accel_ok && dead.n_accel == 0 && dead.n_cpu == seeds.size(),
+              "calibrate_marks_dead_device");
+        hb_ctx_inject_fault(gpu.context(), HB_FAULT_NONE, 0);
+        check(gpu.run(r).results == want.results, "fault_reset");
+    }
     std::printf("%d failure(s)\n", g_fail);
     return g_fail;
 }

@@ -31,11 +31,12 @@ EXPORTED = (
     "hb_run_batch_multi", "hb_fp64_peak", "hb_ctx_set_kernel", "hb_check_fast_math",
     "hb_last_launch_stats", "hb_run_ea", "hb_eval_device", "hb_ea_init_genomes",
     "hb_ea_select_vary", "hb_host_alloc", "hb_host_free", "hb_last_fail_steps",
-    "hb_ctx_set_zero_copy", "hb_ctx_set_precision", "hb_work_counter",
+    "hb_ctx_set_zero_copy", "hb_ctx_set_precision", "hb_work_counter", "hb_ctx_inject_fault",
 )
 
 HB_KERNEL_AUTO, HB_KERNEL_GENERIC = 0, 1
 HB_PRECISION_FP64, HB_PRECISION_FP32 = 0, 1
+HB_FAULT_NONE, HB_FAULT_BLOWUP, HB_FAULT_DEVICE = 0, 1, 2
 
 
 class PhaseProfile(C.Structure):
@@ -96,6 +97,7 @@ def _load():
         "hb_ctx_set_zero_copy": (i32, [vp, i32]),
         "hb_ctx_set_precision": (i32, [vp, i32]),
         "hb_work_counter": (i32, [vp, P(u64)]),
+        "hb_ctx_inject_fault": (i32, [vp, i32, u64]),
         "hb_check_fast_math": (i32, [vp, vp, vp, sz, P(u64), P(u64), P(u64), P(u64)]),
     }
     for name, (res, args) in sig.items():

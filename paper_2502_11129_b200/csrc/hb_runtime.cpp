@@ -75,32 +75,51 @@ public:
             fn(0, total);
             return;
         }
+        Job job;
         {
             std::lock_guard<std::mutex> g(m_);
-            fn_ = &fn;
-            total_ = total;
-            parts_ = parts;
-            next_.store(0);
-            done_.store(0);
+            job = Job{&fn, total, parts, ++job_id_};
+            job_ = job;
+            done_.store(0, std::memory_order_relaxed);
+            // publishing the job id in the claim word opens the job's parts
+            next_.store(job.id << 32, std::memory_order_release);
             gen_.fetch_add(1);
         }
         cv_.notify_all();
-        work();
-        while (done_.load(std::memory_order_acquire) != parts_) {
+        work(job);
+        while (done_.load(std::memory_order_acquire) < parts) {
         }
         std::lock_guard<std::mutex> g(m_);
-        fn_ = nullptr;
+        job_.fn = nullptr;
     }
 
 private:
-    void work() {
+    // One fork/join job.  Workers copy it under the lock and claim parts
+    // through `next_`, whose high 32 bits hold the job id and low 32 bits the
+    // next part: a worker holding an older job's copy finds a different id
+    // and claims nothing, so a late wake-up can never take (and run twice) a
+    // part of the current job, and done_ counts exactly the current job's
+    // parts.
+    struct Job {
+        const std::function<void(size_t, size_t)>* fn = nullptr;
+        size_t total = 0;
+        int parts = 0;
+        uint64_t id = 0;
+    };
+    void work(const Job& job) {
         for (;;) {
-            const int part = next_.fetch_add(1);
-            if (part >= parts_) break;
-            const size_t chunk = total_ / parts_, extra = total_ % parts_;
+            uint64_t v = next_.load(std::memory_order_acquire);
+            int part;
+            for (;;) {
+                if ((v >> 32) != (job.id & 0xffffffffu)) return;
+                part = static_cast<int>(v & 0xffffffffu);
+                if (part >= job.parts) return;
+                if (next_.compare_exchange_weak(v, v + 1, std::memory_order_acq_rel)) break;
+            }
+            const size_t chunk = job.total / job.parts, extra = job.total % job.parts;
             const size_t b = part * chunk + std::min<size_t>(part, extra);
             const size_t e = b + chunk + (static_cast<size_t>(part) < extra ? 1 : 0);
-            (*fn_)(b, e);
+            (*job.fn)(b, e);
             done_.fetch_add(1, std::memory_order_release);
         }
     }
@@ -118,20 +137,21 @@ private:
             }
             seen = gen_.load();
             if (stop_.load()) return;
-            std::unique_lock<std::mutex> lk(m_);
-            if (!fn_) continue;
-            lk.unlock();
-            work();
+            Job job;
+            {
+                std::lock_guard<std::mutex> lk(m_);
+                job = job_;
+            }
+            if (job.fn) work(job);
         }
     }
     int n_;
     std::vector<std::thread> workers_;
     std::mutex m_;
     std::condition_variable cv_;
-    const std::function<void(size_t, size_t)>* fn_ = nullptr;
-    size_t total_ = 0;
-    int parts_ = 0;
-    std::atomic<int> next_{0};
+    Job job_;               // the current job (guarded by m_)
+    uint64_t job_id_ = 0;   // guarded by m_
+    std::atomic<uint64_t> next_{0};
     std::atomic<int> done_{0};
     std::atomic<uint64_t> gen_{0};
     std::atomic<bool> stop_{false};
@@ -343,6 +363,8 @@ struct hb_ctx {
     size_t last_n = 0;
     bool counters_dirty = true;  // device counters need a reset before the next launch
     bool zero_copy = true;       // Box: read seeds / write results through host mappings
+    int fault_mode = HB_FAULT_NONE;  // hb_ctx_inject_fault (test seam)
+    uint64_t fault_seed = 0;
 
     hb_status fail(hb_status st, const std::string& msg) {
         err = msg;
@@ -637,7 +659,10 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
         return set_global(HB_NO_DEVICE, "cudaGetDeviceProperties failed");
-    if (prop.major != 10)
+    // The library carries sm_100a code only (no PTX): arch-specific code loads
+    // on compute capability 10.0 alone, so anything else (e.g. sm_103) would
+    // create a context whose every launch fails with no-kernel-image.
+    if (prop.major != 10 || prop.minor != 0)
         return set_global(HB_NO_DEVICE, "device is sm_" + std::to_string(prop.major) +
                                             std::to_string(prop.minor) +
                                             "; this build targets sm_100a only");
@@ -811,10 +836,32 @@ static hb_status run_box_zero_copy(hb_ctx* c, const uint64_t* dseeds, hb_variant
     return HB_OK;
 }
 
+// HB_FAULT_BLOWUP: the injected variants' records become blow-ups at step 1
+// (host side, after the real batch; the failure steps of the batch are kept
+// in h_fail for hb_last_fail_steps).
+static void apply_blowup_fault(hb_ctx* c, const uint64_t* seeds, size_t n, hb_variant_result* out,
+                               uint64_t* fail_step, bool* any) {
+    if (c->fault_mode != HB_FAULT_BLOWUP) return;
+    bool hit = false;
+    for (size_t i = 0; i < n && !hit; ++i) hit = seeds[i] == c->fault_seed;
+    if (!hit) return;
+    if (!*any) std::memset(c->h_fail, 0, n * sizeof(uint64_t));
+    for (size_t i = 0; i < n; ++i) {
+        if (seeds[i] != c->fault_seed) continue;
+        if (c->h_fail[i] == 0) ++c->last_failed;
+        out[i] = hb_variant_result{seeds[i], 0.0, 0, 1};
+        c->h_fail[i] = 1;
+        if (fail_step) fail_step[i] = 1;
+    }
+    *any = true;
+}
+
 hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
                        hb_variant_result* out, uint64_t* fail_step, double* wall_time_s) {
     const auto t0 = std::chrono::steady_clock::now();
     HB_TRY(validate(c, kind, seeds, n, steps, out));
+    if (c->fault_mode == HB_FAULT_DEVICE)
+        return c->fail(HB_CUDA_ERROR, "injected device fault (hb_ctx_inject_fault)");
     if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO && c->zero_copy) {
         Trace tr("ptrs");
         void* ds = mapped_device_ptr(seeds);
@@ -824,6 +871,7 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
             bool any = false;
             HB_TRY(run_box_zero_copy(c, static_cast<const uint64_t*>(ds),
                                      static_cast<hb_variant_result*>(dout), n, steps, fail_step, &any));
+            apply_blowup_fault(c, seeds, n, out, fail_step, &any);
             if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
             if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
             return HB_OK;
@@ -833,8 +881,16 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
     HB_TRY(launch(c, kind, n, steps, hb::kSimDt, c->staged_from_seeds, nullptr));
     bool any = false;
     HB_TRY(fetch(c, n, out, fail_step, &any));
+    apply_blowup_fault(c, seeds, n, out, fail_step, &any);
     if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_ctx_inject_fault(hb_ctx* c, int mode, uint64_t seed) {
+    if (!c || mode < HB_FAULT_NONE || mode > HB_FAULT_DEVICE) return set_global(HB_INVALID_ARG, "bad arguments");
+    c->fault_mode = mode;
+    c->fault_seed = seed;
     return HB_OK;
 }
 
@@ -1362,11 +1418,20 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
     }
     cudaEvent_t ev_ready = c0->ea_ev[0], e0 = c0->ea_ev[1], e2 = c0->ea_ev[2];
 
+    // a non-finite or non-positive device time marks a device without a
+    // share (dead to the splitter, as a failed calibration)
     std::vector<double> times(count, 1.0);
-    if (device_times) for (int d = 0; d < count; ++d) times[d] = device_times[d];
+    std::vector<int> alive(count, 1);
+    if (device_times)
+        for (int d = 0; d < count; ++d) {
+            times[d] = device_times[d];
+            alive[d] = std::isfinite(times[d]) && times[d] > 0.0;
+        }
+    if (std::find(alive.begin(), alive.end(), 1) == alive.end())
+        return c0->fail(HB_INVALID_ARG, "run_ea: no device has a finite positive time");
     auto shares_for = [&](size_t n) {
         std::vector<uint64_t> sh(count);
-        hb_plan_allocation_n(times.data(), nullptr, count, n, sh.data());
+        hb_plan_allocation_n(times.data(), alive.data(), count, n, sh.data());
         return sh;
     };
     auto snapshot = [&](int cur, uint64_t g) -> hb_status {

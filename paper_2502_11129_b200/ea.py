@@ -155,10 +155,18 @@ def run_ea_native(kind: ModelKind, population_size: int, generations: int, steps
     cnt = len(ctxs)
     handles = (C.c_void_p * cnt)(*[c.handle for c in ctxs])
     times = None
+    if device_times is None and isinstance(executor, MultiGpuExecutor):
+        # the executor's calibration: measured per-device probe times, else
+        # its fixed shares read as throughputs (time ~ 1 / share; a device
+        # with no share gets an infinite time, hence no offspring)
+        if executor.device_times is not None:
+            device_times = executor.device_times
+        elif executor.shares is not None:
+            device_times = [1.0 / s if s > 0 else np.inf for s in executor.shares]
     if device_times is not None:
         times = np.ascontiguousarray(device_times, dtype=np.float64)
-    elif isinstance(executor, MultiGpuExecutor) and executor.shares is not None:
-        times = None
+        if len(times) != cnt:
+            raise ValueError("run_ea: one device time per context required")
     # page-locked (recycled) outputs: the final population is DMA'd straight in
     gen = _lib.pinned.empty(population_size, np.uint64)
     fit = _lib.pinned.empty(population_size, np.float64)

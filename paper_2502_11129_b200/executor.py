@@ -207,6 +207,12 @@ class DeviceContext:
         self.check(lib.hb_work_counter(self.handle, C.byref(v)), "hb_work_counter")
         return int(v.value)
 
+    def inject_fault(self, mode: int, seed: int = 0) -> None:
+        """Test seam (hb_ctx_inject_fault): HB_FAULT_BLOWUP reports the variants
+        with this seed as blown up at step 1; HB_FAULT_DEVICE makes every
+        hb_run_batch fail as a dead device; HB_FAULT_NONE resets."""
+        self.check(lib.hb_ctx_inject_fault(self.handle, int(mode), int(seed)), "hb_ctx_inject_fault")
+
     def set_precision(self, precision: int) -> None:
         """_lib.HB_PRECISION_FP64 (bit-exact product path, default) or
         _lib.HB_PRECISION_FP32 (throughput mode: float-float
@@ -314,7 +320,9 @@ class MultiGpuExecutor(BatchExecutor):
 
     def __init__(self, devices: Sequence[int], host_threads: int = 0):
         self.ctxs = [DeviceContext(d, host_threads) for d in devices]
-        self.shares = None
+        self.shares = None        # fixed per-device shares (sum = batch size), or
+        self.device_times = None  # calibrated per-device probe times -> plan_allocation_n
+        self.device_ok = None     # calibration's liveness flags (None = all alive)
         self.last_device_walls = None
 
     def name(self) -> str:

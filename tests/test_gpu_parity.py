@@ -267,6 +267,48 @@ def test_exact_replay_path_blowup_states(gpu, gpu_generic):
     assert np.array_equal(a[2][ok], b[2][ok]) and np.array_equal(a[3][ok], b[3][ok])
 
 
+def test_humanoid_blowup_final_state(gpu, gpu_generic):
+    """A humanoid pair that blows up mid-horizon keeps stepping in lockstep
+    with its warp (the rung shuffles need both lanes) but its state freezes
+    after the failing step: final_soa is the state simulate() holds when
+    step() throws, as the generic kernel (which stops) reports it."""
+    kind, N = 3, 64
+    seeds = np.arange(N, dtype=np.uint64)
+    soa = hb.build_states(kind, seeds)
+    n = 32
+    pos = soa[: 3 * n].T.reshape(N, n, 3).copy()
+    vel = soa[3 * n: 6 * n].T.reshape(N, n, 3).copy()
+    rest = soa[6 * n:].T.copy()
+    pos[1::4, :, 0] += 999000.0  # drifts past |x| = 1e6 after ~1000 steps
+    vel[1::4, :, 0] = 1000.0
+    a = gpu.run_states(kind, pos, vel, rest, steps=1500, seeds=seeds)
+    b = gpu_generic.run_states(kind, pos, vel, rest, steps=1500, seeds=seeds)
+    assert np.array_equal(a[1], b[1])
+    failed = a[1] != 0
+    assert failed.sum() == N // 4 and np.all(a[1][failed] > 500) and np.all(a[1][failed] < 1500)
+    assert np.array_equal(a[0][~failed], b[0][~failed])
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
+
+
+def test_box_nan_state_fails_at_step_one(gpu):
+    """A NaN x / y / velocity coordinate (which p.z >= 0 does not catch) keeps
+    the warp out of the proven Box phases: the blow-up is reported at step 1,
+    as the reference's end-of-step check (simkernel.cpp:165-169) reports it."""
+    N = 64
+    seeds = np.arange(N, dtype=np.uint64)
+    soa = hb.build_states(0, seeds)
+    pos = soa[:3].T.reshape(N, 1, 3).copy()
+    vel = soa[3:6].T.reshape(N, 1, 3).copy()
+    pos[3, 0, 0] = np.nan
+    vel[9, 0, 1] = np.nan
+    vel[17, 0, 0] = np.nan
+    out, fail, fp, fv = gpu.run_states(0, pos, vel, np.zeros((N, 0)), steps=200, seeds=seeds)
+    assert list(np.nonzero(fail)[0]) == [3, 9, 17] and np.all(fail[[3, 9, 17]] == 1)
+    ok = fail == 0
+    want = O.simulate_batch(0, seeds, 200).results
+    assert np.array_equal(out[ok], want[ok])
+
+
 def test_box_zero_copy_path_equals_staged(gpu):
     """Box with pinned seeds + pinned results runs zero-copy (seeds read and
     results written through the host mapping); results identical to the
