@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HBGPU_ABI_VERSION 1
+#define HBGPU_ABI_VERSION 2
 
 /* hetbench::ModelKind (include/hetbench/simkernel.hpp:14) — same ordinals.
  * HB_CPG_HINGE (4) is NOT a reference model: the "Revolve2-style modular
@@ -228,15 +228,45 @@ hb_status hb_plan_allocation_n(const double* t_s, const int* ok, int count, uint
                                uint64_t* shares);
 
 /* ---- multi-device executor -------------------------------------------------
- * One context and one host thread per device; the batch is cut into
- * contiguous slices (shares[d] variants to device d, in device order, as
+ * One context and one persistent host thread per device; the batch is cut
+ * into contiguous slices (shares[d] variants to device d, in device order, as
  * run_hybrid slices seeds at scheduler.cpp:122-127) and merged in seed order.
  * shares == NULL splits evenly.  per_device_wall_s (nullable, `count`
- * entries) receives each device's run wall time. */
+ * entries) receives each device's run wall time.
+ * Degraded mode (the N-way form of run_hybrid's re-dispatch,
+ * scheduler.cpp:162-183): a device whose slice fails with anything but
+ * HB_BLOWUP_PARTIAL is dead for the rest of the call and its slice is
+ * re-planned over the surviving devices with hb_plan_allocation_n (ok = 0 for
+ * the dead ones, the survivors weighted by their original shares); the
+ * results are complete and identical to a healthy run.  device_ok (nullable,
+ * `count` entries) = 1 for devices that finished their work, *degraded
+ * (nullable) = 1 if any device died.  Only when every device fails does the
+ * call fail (with the first device's status). */
 hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* shares, int kind,
                              const uint64_t* seeds, size_t n, uint64_t steps,
                              hb_variant_result* out, uint64_t* fail_step,
-                             double* per_device_wall_s, double* wall_time_s);
+                             double* per_device_wall_s, double* wall_time_s,
+                             int* device_ok, int* degraded);
+
+/* ---- calibration (the paper's calibrate step, scheduler.cpp:30-56, on
+ * devices) ------------------------------------------------------------------
+ * Times the probe batch (seeds 0..probe_n-1 of `kind` through `steps` steps)
+ * on every context concurrently with CUDA events on the context's stream:
+ * the probe is relaunched back to back until one sample spans >= 5 ms, and
+ * t_s[d] is the median per-launch time of `repeats` (>= 1; 5 recommended)
+ * such samples, spread[d] (nullable) their relative range (max - min) /
+ * median.  A device whose probe fails gets ok[d] = 0 and t_s[d] = 0 (dead to
+ * the splitter, like a throwing back-end in calibrate); HB_INVALID_ARG only
+ * for bad arguments, otherwise HB_OK if at least one device survived. */
+hb_status hb_calibrate(hb_ctx* const* ctxs, int count, int kind, uint64_t probe_n, uint64_t steps,
+                       int repeats, double* t_s, double* spread, int* ok);
+/* Equal devices get equal shares: if the alive devices' times agree within
+ * max(their largest measured spread, min_rel_tol) (relative to the fastest),
+ * every alive device's time becomes their mean, so plan_allocation_n splits
+ * evenly instead of amplifying measurement noise; otherwise the times are
+ * returned unchanged.  Returns 1 if it snapped.  ok / spread nullable. */
+int hb_snap_equal_times(const double* t_s, const double* spread, const int* ok, int count,
+                        double min_rel_tol, double* out_t_s);
 
 /* ---- FP64 pipe peak probe (roofline denominator) ---------------------------
  * Times a dependent-chain-free DADD/DMUL stream on the context's device and

@@ -13,7 +13,8 @@ from .executor import (ALL_MODELS, BatchExecutor, BatchFailure, BatchRequest, Ba
                        validate_request)
 from .scheduler import (AllocationPlan, CalibrationProfile, HybridResult, calibrate, calibrate_n,
                         format_plan, naive_sum, plan_allocation, plan_allocation_n,
-                        plan_allocation_optimal, run_hybrid, run_sharded)
+                        plan_allocation_optimal, run_hybrid, run_sharded, ShardedResult,
+                        snap_equal_times)
 from .ea import (EaResult, PhaseProfile, Population, report_profile, rng_at, run_ea,
                  run_ea_native, stable_order_desc)
 

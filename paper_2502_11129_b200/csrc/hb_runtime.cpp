@@ -157,6 +157,79 @@ private:
     std::atomic<bool> stop_{false};
 };
 
+// One persistent host thread per device context for the multi-device calls
+// (hb_run_batch_multi, the multi-context generation loop): each device gets
+// its job handed over instead of a std::thread created and joined per call /
+// per generation.  The worker spins briefly before sleeping, so back-to-back
+// jobs (one per generation) are picked up in about a microsecond.
+class DeviceWorker {
+public:
+    DeviceWorker() : th_([this] { loop(); }) {}
+    ~DeviceWorker() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+            seq_.fetch_add(1);
+        }
+        cv_.notify_all();
+        th_.join();
+    }
+    void submit(std::function<void()> job) {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            job_ = std::move(job);
+            done_.store(false, std::memory_order_relaxed);
+            seq_.fetch_add(1, std::memory_order_release);
+        }
+        cv_.notify_all();
+    }
+    void wait() {
+        auto t0 = std::chrono::steady_clock::now();
+        while (!done_.load(std::memory_order_acquire)) {
+            if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                std::unique_lock<std::mutex> lk(m_);
+                done_cv_.wait(lk, [&] { return done_.load(); });
+                return;
+            }
+        }
+    }
+
+private:
+    void loop() {
+        uint64_t seen = 0;
+        for (;;) {
+            auto t0 = std::chrono::steady_clock::now();
+            while (seq_.load(std::memory_order_acquire) == seen) {
+                if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(200)) {
+                    std::unique_lock<std::mutex> lk(m_);
+                    cv_.wait(lk, [&] { return seq_.load() != seen; });
+                    break;
+                }
+            }
+            std::function<void()> job;
+            {
+                std::lock_guard<std::mutex> g(m_);
+                seen = seq_.load();
+                if (stop_) return;
+                job = std::move(job_);
+            }
+            if (job) job();
+            {
+                std::lock_guard<std::mutex> g(m_);
+                done_.store(true, std::memory_order_release);
+            }
+            done_cv_.notify_all();
+        }
+    }
+    std::mutex m_;
+    std::condition_variable cv_, done_cv_;
+    std::function<void()> job_;
+    std::atomic<uint64_t> seq_{0};
+    std::atomic<bool> done_{true};
+    bool stop_ = false;
+    std::thread th_;
+};
+
 int default_host_threads() {
     unsigned hc = std::thread::hardware_concurrency();
     return static_cast<int>(std::min(64u, std::max(1u, hc)));
@@ -308,6 +381,7 @@ struct hb_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     ThreadPool* pool = nullptr;
+    DeviceWorker* worker = nullptr;  // this context's thread in multi-device calls
     int host_threads = 0;
 
     // device buffers
@@ -431,6 +505,11 @@ hb_status ensure_capacity(hb_ctx* c, int kind, size_t n, bool need_init) {
         c->h_n_cap = cap;
     }
     return HB_OK;
+}
+
+DeviceWorker& worker_of(hb_ctx* c) {
+    if (!c->worker) c->worker = new DeviceWorker();
+    return *c->worker;
 }
 
 ThreadPool& pool_of(hb_ctx* c) {
@@ -690,6 +769,7 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
 
 void hb_ctx_destroy(hb_ctx* c) {
     if (!c) return;
+    delete c->worker;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_init); cudaFree(c->d_trig); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
@@ -1037,15 +1117,27 @@ hb_status hb_plan_allocation_n(const double* t_s, const int* ok, int count, uint
     return HB_OK;
 }
 
+// N-way run_hybrid (scheduler.cpp:113-211) over device contexts: contiguous
+// slices in device order, one persistent worker thread per device, merged in
+// seed order.  A device that fails its slice with anything but a blow-up
+// (HB_BLOWUP_PARTIAL is the batch's own result: re-running it elsewhere
+// reproduces it) is dead for the rest of the call, and its slice is
+// re-planned over the surviving devices by hb_plan_allocation_n (ok = 0 for
+// the dead), in proportion to the shares the survivors were given — the N-way
+// form of the reference's re-dispatch (:162-183); the result is degraded.
 hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* shares, int kind,
                              const uint64_t* seeds, size_t n, uint64_t steps,
                              hb_variant_result* out, uint64_t* fail_step,
-                             double* per_device_wall_s, double* wall_time_s) {
+                             double* per_device_wall_s, double* wall_time_s,
+                             int* device_ok, int* degraded) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!ctxs || count < 1) return set_global(HB_INVALID_ARG, "no contexts");
+    for (int d = 0; d < count; ++d)
+        if (!ctxs[d]) return set_global(HB_INVALID_ARG, "null context");
     if (!valid_kind(kind)) return set_global(HB_INVALID_ARG, "unknown model kind");
     if (n == 0) return set_global(HB_INVALID_ARG, "batch request: seeds must be non-empty");
     if (steps < 1) return set_global(HB_INVALID_ARG, "batch request: steps must be >= 1");
+    if (!seeds || !out) return set_global(HB_INVALID_ARG, "null buffer");
     std::vector<uint64_t> sh(count);
     if (shares) {
         uint64_t sum = 0;
@@ -1054,31 +1146,188 @@ hb_status hb_run_batch_multi(hb_ctx* const* ctxs, int count, const uint64_t* sha
     } else {
         for (int d = 0; d < count; ++d) sh[d] = n / count + (static_cast<uint64_t>(d) < n % count ? 1 : 0);
     }
-    std::vector<hb_status> st(count, HB_OK);
+    // re-dispatch weights: a device's original share is its throughput
+    std::vector<double> weight(count);
+    for (int d = 0; d < count; ++d) weight[d] = sh[d] > 0 ? 1.0 / static_cast<double>(sh[d]) : 1.0;
+    std::vector<int> alive(count, 1);
     std::vector<double> walls(count, 0.0);
-    std::vector<std::thread> th;
-    size_t begin = 0;
-    for (int d = 0; d < count; ++d) {
-        const size_t b = begin, len = sh[d];
-        begin += len;
-        if (len == 0) continue;
-        th.emplace_back([&, d, b, len] {
-            st[d] = hb_run_batch(ctxs[d], kind, seeds + b, len, steps, out + b,
-                                 fail_step ? fail_step + b : nullptr, &walls[d]);
-        });
+    std::vector<hb_status> st(count, HB_OK);
+    std::vector<std::string> err(count);
+    struct Slice { size_t b, len; };
+    std::vector<std::vector<Slice>> work(count);
+    {
+        size_t begin = 0;
+        for (int d = 0; d < count; ++d) {
+            if (sh[d]) work[d].push_back({begin, sh[d]});
+            begin += sh[d];
+        }
     }
-    for (auto& t : th) t.join();
+    bool blow = false, lost = false;
+    std::string first_err;
+    hb_status first_st = HB_OK;
+    for (;;) {
+        std::vector<int> busy;
+        for (int d = 0; d < count; ++d) {
+            if (work[d].empty()) continue;
+            busy.push_back(d);
+            worker_of(ctxs[d]).submit([&, d] {
+                st[d] = HB_OK;
+                for (const Slice& s : work[d]) {
+                    double w = 0.0;
+                    const hb_status r = hb_run_batch(ctxs[d], kind, seeds + s.b, s.len, steps, out + s.b,
+                                                     fail_step ? fail_step + s.b : nullptr, &w);
+                    walls[d] += w;
+                    if (r == HB_BLOWUP_PARTIAL) {
+                        if (st[d] == HB_OK) st[d] = r;
+                    } else if (r != HB_OK) {
+                        st[d] = r;
+                        err[d] = hb_last_error(ctxs[d]);
+                        return;
+                    }
+                }
+            });
+        }
+        if (busy.empty()) break;
+        for (int d : busy) worker_of(ctxs[d]).wait();
+        std::vector<Slice> orphans;
+        for (int d : busy) {
+            if (st[d] == HB_BLOWUP_PARTIAL) blow = true;
+            if (st[d] == HB_OK || st[d] == HB_BLOWUP_PARTIAL) {
+                work[d].clear();
+                continue;
+            }
+            if (first_st == HB_OK) {
+                first_st = st[d];
+                first_err = "device " + std::to_string(d) + ": " + err[d];
+            }
+            alive[d] = 0;
+            lost = true;
+            orphans.insert(orphans.end(), work[d].begin(), work[d].end());
+            work[d].clear();
+        }
+        if (orphans.empty()) break;
+        if (std::find(alive.begin(), alive.end(), 1) == alive.end()) {
+            if (device_ok) for (int d = 0; d < count; ++d) device_ok[d] = 0;
+            return set_global(first_st, "all devices failed; " + first_err);
+        }
+        for (const Slice& o : orphans) {
+            std::vector<uint64_t> part(count);
+            hb_plan_allocation_n(weight.data(), alive.data(), count, o.len, part.data());
+            size_t b = o.b;
+            for (int d = 0; d < count; ++d) {
+                if (part[d]) work[d].push_back({b, part[d]});
+                b += part[d];
+            }
+        }
+    }
     if (per_device_wall_s)
         for (int d = 0; d < count; ++d) per_device_wall_s[d] = walls[d];
+    if (device_ok)
+        for (int d = 0; d < count; ++d) device_ok[d] = alive[d];
+    if (degraded) *degraded = lost ? 1 : 0;
     if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
-    bool blow = false;
-    for (int d = 0; d < count; ++d) {
-        if (st[d] == HB_BLOWUP_PARTIAL) blow = true;
-        else if (st[d] != HB_OK) return set_global(st[d], std::string("device ") + std::to_string(d) +
-                                                              ": " + hb_last_error(ctxs[d]));
-    }
     if (blow) return set_global(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
     return HB_OK;
+}
+
+// Probe timing on one context (hb_calibrate): stage seeds 0..probe_n-1 once,
+// then `repeats` samples of back-to-back launches bracketed by CUDA events on
+// the context's stream, each sample >= 5 ms.
+static hb_status calibrate_one(hb_ctx* c, int kind, uint64_t probe_n, uint64_t steps, int repeats,
+                               double* t, double* spread) {
+    std::vector<uint64_t> seeds(probe_n);
+    for (uint64_t i = 0; i < probe_n; ++i) seeds[i] = i;
+    HB_TRY(validate(c, kind, seeds.data(), probe_n, steps, seeds.data()));
+    if (c->fault_mode == HB_FAULT_DEVICE)
+        return c->fail(HB_CUDA_ERROR, "injected device fault (hb_ctx_inject_fault)");
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    HB_TRY(stage_inputs(c, kind, seeds.data(), probe_n));
+    cudaEvent_t e0, e1;
+    HB_TRY(c->cuda(cudaEventCreate(&e0), "event"));
+    if (cudaEventCreate(&e1) != cudaSuccess) {
+        cudaEventDestroy(e0);
+        return c->fail(HB_CUDA_ERROR, "event");
+    }
+    auto sample = [&](int k, double* ms) -> hb_status {
+        HB_TRY(c->cuda(cudaEventRecord(e0, c->stream), "event record"));
+        for (int j = 0; j < k; ++j)
+            HB_TRY(launch(c, kind, probe_n, steps, hb::kSimDt, c->staged_from_seeds, nullptr));
+        HB_TRY(c->cuda(cudaEventRecord(e1, c->stream), "event record"));
+        HB_TRY(c->cuda(cudaEventSynchronize(e1), "event sync"));
+        float f = 0.f;
+        HB_TRY(c->cuda(cudaEventElapsedTime(&f, e0, e1), "event time"));
+        *ms = static_cast<double>(f) / k;
+        return HB_OK;
+    };
+    hb_status st = HB_OK;
+    double one = 0.0;
+    std::vector<double> v;
+    if ((st = sample(1, &one)) == HB_OK && (st = sample(1, &one)) == HB_OK) {  // warm-up, then size
+        const int k = static_cast<int>(std::min(4096.0, std::max(1.0, std::ceil(5.0 / std::max(one, 1e-4)))));
+        for (int r = 0; r < repeats && st == HB_OK; ++r) {
+            double ms = 0.0;
+            st = sample(k, &ms);
+            v.push_back(ms);
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    c->counters_dirty = true;  // the probe's launches added to the counters
+    c->staged_kind = -1;
+    if (st != HB_OK) return st;
+    std::sort(v.begin(), v.end());
+    const size_t m = v.size();
+    const double med = m % 2 ? v[m / 2] : 0.5 * (v[m / 2 - 1] + v[m / 2]);
+    *t = 1e-3 * med;
+    *spread = med > 0.0 ? (v.back() - v.front()) / med : 0.0;
+    return HB_OK;
+}
+
+hb_status hb_calibrate(hb_ctx* const* ctxs, int count, int kind, uint64_t probe_n, uint64_t steps,
+                       int repeats, double* t_s, double* spread, int* ok) {
+    if (!ctxs || count < 1 || !t_s || !ok || repeats < 1) return set_global(HB_INVALID_ARG, "bad arguments");
+    if (probe_n < 1) return set_global(HB_INVALID_ARG, "calibrate: probe_n must be >= 1");
+    if (!valid_kind(kind)) return set_global(HB_INVALID_ARG, "unknown model kind");
+    if (steps < 1) return set_global(HB_INVALID_ARG, "batch request: steps must be >= 1");
+    for (int d = 0; d < count; ++d)
+        if (!ctxs[d]) return set_global(HB_INVALID_ARG, "null context");
+    std::vector<double> sp(count, 0.0);
+    std::vector<hb_status> st(count, HB_OK);
+    for (int d = 0; d < count; ++d)
+        worker_of(ctxs[d]).submit([&, d] {
+            st[d] = calibrate_one(ctxs[d], kind, probe_n, steps, repeats, &t_s[d], &sp[d]);
+        });
+    int alive = 0;
+    for (int d = 0; d < count; ++d) {
+        worker_of(ctxs[d]).wait();
+        ok[d] = st[d] == HB_OK;
+        if (!ok[d]) t_s[d] = 0.0, sp[d] = 0.0;
+        alive += ok[d];
+        if (spread) spread[d] = sp[d];
+    }
+    if (!alive) return set_global(HB_CUDA_ERROR, "calibrate: all back-ends failed");
+    return HB_OK;
+}
+
+int hb_snap_equal_times(const double* t_s, const double* spread, const int* ok, int count,
+                        double min_rel_tol, double* out_t_s) {
+    if (!t_s || !out_t_s || count < 1) return 0;
+    double lo = 0.0, hi = 0.0, sum = 0.0, tol = min_rel_tol;
+    int alive = 0;
+    for (int d = 0; d < count; ++d) {
+        out_t_s[d] = t_s[d];
+        if (ok && !ok[d]) continue;
+        if (!(t_s[d] > 0.0) || !std::isfinite(t_s[d])) return 0;
+        lo = alive ? std::min(lo, t_s[d]) : t_s[d];
+        hi = alive ? std::max(hi, t_s[d]) : t_s[d];
+        sum += t_s[d];
+        if (spread) tol = std::max(tol, spread[d]);
+        ++alive;
+    }
+    if (alive < 2 || (hi - lo) / lo > tol) return 0;
+    for (int d = 0; d < count; ++d)
+        if (!ok || ok[d]) out_t_s[d] = sum / alive;
+    return 1;
 }
 
 hb_status hb_fp64_peak(hb_ctx* c, double* ops_per_s, double* ms) {

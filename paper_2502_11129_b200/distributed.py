@@ -23,31 +23,57 @@ from .scheduler import plan_allocation_n
 
 def shard_bounds(n: int, world: int, times=None) -> np.ndarray:
     """Contiguous per-rank slice bounds [b_0 = 0, ..., b_world = n] from the
-    N-way splitter over calibrated per-rank times (None = equal ranks)."""
+    N-way splitter over calibrated per-rank times (None = equal ranks; a
+    time of 0 = a rank that failed calibration, which gets no share)."""
     shares = plan_allocation_n(list(times) if times is not None else [1.0] * world, n)
     return np.concatenate([[0], np.cumsum(shares)]).astype(np.int64)
 
 
 def calibrate_ranks(kind: ModelKind, steps: int, probe_n: int, executor: BatchExecutor, dist,
-                    repeats: int = 3):
+                    repeats: int = 5, snap_tol: float = 0.01):
     """The paper's calibration step (scheduler.cpp:30-56) across the ranks of
-    the default group: every rank times the same probe (seeds 0..probe_n-1,
-    best of `repeats` drop-in calls, wall_time_s) on its own device at once,
-    and the per-rank times are all-gathered, so every rank holds the same
-    times — the input of the N-way splitter (plan_allocation_n), which then
-    gives each rank a share in proportion to its measured throughput."""
+    the default group: every rank times the same probe (seeds 0..probe_n-1)
+    on its own device at once and the per-rank (time, spread, ok) triples are
+    all-gathered, so every rank holds the same times — the input of the N-way
+    splitter (plan_allocation_n / shard_bounds), which gives each rank a share
+    in proportion to its measured throughput.
+
+    A GPU rank times the probe with CUDA events on its context's stream
+    (hb_calibrate: relaunched until a sample spans >= 5 ms, median of
+    `repeats` samples, relative spread); any other back-end reports the
+    median of `repeats` drop-in wall times.  A rank whose back-end throws is
+    dead to the splitter (time 0, no share), as a throwing back-end is to
+    calibrate (scheduler.cpp:40-49) — the job goes on without it.  Times that
+    agree within the largest measured spread (at least snap_tol) snap to
+    equal (snap_equal_times): identical GPUs get identical shares instead of
+    a split that follows measurement noise."""
     import torch
+
+    from .executor import GpuExecutor
+    from .scheduler import median_and_spread, snap_equal_times
     if probe_n < 1:
         raise ValueError("calibrate: probe_n must be >= 1")
-    req = BatchRequest(kind, np.arange(probe_n, dtype=np.uint64), steps)
-    best = min(executor.run(req).wall_time_s for _ in range(max(1, repeats)))
+    try:
+        if isinstance(executor, GpuExecutor):
+            t, sp = executor.ctx.calibrate(kind, steps, probe_n, repeats)
+        else:
+            req = BatchRequest(kind, np.arange(probe_n, dtype=np.uint64), steps)
+            t, sp = median_and_spread([executor.run(req).wall_time_s for _ in range(max(1, repeats))])
+        ok = 1.0
+    except Exception:  # noqa: BLE001 - a failing rank is dead, not fatal
+        t, sp, ok = 0.0, 0.0, 0.0
     world = dist.get_world_size()
-    mine = torch.tensor([best], dtype=torch.float64)
+    mine = torch.tensor([t, sp, ok], dtype=torch.float64)
     if dist.get_backend() == "nccl":
         mine = mine.cuda()
     parts = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(parts, mine)
-    return [float(t.item()) for t in parts]
+    rows = [[float(x) for x in p.cpu()] for p in parts]
+    oks = [r[2] > 0.5 for r in rows]
+    if not any(oks):
+        raise RuntimeError("calibrate: all ranks failed")
+    times = snap_equal_times([r[0] for r in rows], [r[1] for r in rows], oks, snap_tol)
+    return [t if o else 0.0 for t, o in zip(times, oks)]
 
 
 def evaluate_sharded(kind: ModelKind, genomes: np.ndarray, steps: int, executor: BatchExecutor,

@@ -207,6 +207,19 @@ class DeviceContext:
         self.check(lib.hb_work_counter(self.handle, C.byref(v)), "hb_work_counter")
         return int(v.value)
 
+    def calibrate(self, kind: ModelKind, steps: int, probe_n: int, repeats: int = 5):
+        """hb_calibrate on this context: (median per-launch seconds of the
+        probe, relative spread); raises if the device fails the probe."""
+        t = np.zeros(1)
+        sp = np.zeros(1)
+        ok = np.zeros(1, dtype=np.int32)
+        handles = (C.c_void_p * 1)(self.handle)
+        st = lib.hb_calibrate(C.cast(handles, C.c_void_p), 1, int(kind), int(probe_n), int(steps),
+                              int(repeats), _lib.ptr(t), _lib.ptr(sp), _lib.ptr(ok))
+        if st != _lib.HB_OK or not ok[0]:
+            raise RuntimeError(f"calibrate failed [{st}]: {self.error() or _lib.global_error()}")
+        return float(t[0]), float(sp[0])
+
     def inject_fault(self, mode: int, seed: int = 0) -> None:
         """Test seam (hb_ctx_inject_fault): HB_FAULT_BLOWUP reports the variants
         with this seed as blown up at step 1; HB_FAULT_DEVICE makes every
@@ -324,35 +337,74 @@ class MultiGpuExecutor(BatchExecutor):
         self.device_times = None  # calibrated per-device probe times -> plan_allocation_n
         self.device_ok = None     # calibration's liveness flags (None = all alive)
         self.last_device_walls = None
+        self.last_device_ok = None
+        self.last_degraded = False
 
     def name(self) -> str:
         return f"accel x{len(self.ctxs)}"
 
     def run(self, request: BatchRequest) -> BatchResult:
+        """hb_run_batch_multi: shares from ``shares``, else plan_allocation_n
+        over ``device_times`` / ``device_ok`` (calibrate()), else even.  A
+        device that fails is dropped and its slice re-planned over the
+        survivors (``last_degraded``, ``last_device_ok``)."""
         validate_request(request)
-        seeds = request.seeds
+        seeds = np.ascontiguousarray(request.seeds, dtype=np.uint64)
         n = len(seeds)
         cnt = len(self.ctxs)
         handles = (C.c_void_p * cnt)(*[c.handle for c in self.ctxs])
         sh = None
         if self.shares is not None:
             sh = np.ascontiguousarray(self.shares, dtype=np.uint64)
+        elif self.device_times is not None:
+            from .scheduler import plan_allocation_n
+            sh = np.ascontiguousarray(plan_allocation_n(self.device_times, n, self.device_ok), dtype=np.uint64)
         out = np.empty(n, dtype=RESULT_DTYPE)
         fail = np.empty(n, dtype=np.uint64)
         walls = np.zeros(cnt)
         wall = C.c_double(0)
+        dok = np.zeros(cnt, dtype=np.int32)
+        degraded = C.c_int(0)
         st = lib.hb_run_batch_multi(C.cast(handles, C.c_void_p), cnt,
                                     None if sh is None else _lib.ptr(sh), int(request.kind),
                                     _lib.ptr(seeds), n, int(request.steps), _lib.ptr(out),
-                                    _lib.ptr(fail), _lib.ptr(walls), C.byref(wall))
+                                    _lib.ptr(fail), _lib.ptr(walls), C.byref(wall),
+                                    _lib.ptr(dok), C.byref(degraded))
         if st == _lib.HB_INVALID_ARG:
             raise ValueError(_lib.global_error())
         if st not in (_lib.HB_OK, _lib.HB_BLOWUP_PARTIAL):
             raise RuntimeError(f"hb_run_batch_multi failed [{st}]: {_lib.global_error()}")
         self.last_device_walls = walls
+        self.last_device_ok = [bool(x) for x in dok]
+        self.last_degraded = bool(degraded.value)
         if st == _lib.HB_BLOWUP_PARTIAL:
             _raise_partial(seeds, out, fail)
         return BatchResult(out, wall.value, [])
+
+    def calibrate(self, kind: ModelKind, steps: int, probe_n: int, repeats: int = 5,
+                  snap_tol: float = 0.01):
+        """The paper's calibrate step on every device at once (hb_calibrate:
+        a >= 5 ms probe timed with CUDA events, median of `repeats`), then
+        hb_snap_equal_times (equal devices -> equal shares).  Sets and returns
+        (device_times, device_ok, spreads)."""
+        cnt = len(self.ctxs)
+        handles = (C.c_void_p * cnt)(*[c.handle for c in self.ctxs])
+        t = np.zeros(cnt)
+        sp = np.zeros(cnt)
+        ok = np.zeros(cnt, dtype=np.int32)
+        st = lib.hb_calibrate(C.cast(handles, C.c_void_p), cnt, int(kind), int(probe_n), int(steps),
+                              int(repeats), _lib.ptr(t), _lib.ptr(sp), _lib.ptr(ok))
+        if st == _lib.HB_INVALID_ARG:
+            raise ValueError(_lib.global_error())
+        if st != _lib.HB_OK:
+            raise RuntimeError(_lib.global_error())
+        snapped = np.zeros(cnt)
+        lib.hb_snap_equal_times(_lib.ptr(t), _lib.ptr(sp), _lib.ptr(ok), cnt, float(snap_tol),
+                                _lib.ptr(snapped))
+        self.device_times = [float(x) for x in snapped]
+        self.device_ok = [bool(x) for x in ok]
+        self.shares = None
+        return self.device_times, self.device_ok, [float(x) for x in sp]
 
 
 def build_states(kind: ModelKind, seeds) -> np.ndarray:

@@ -83,22 +83,55 @@ def calibrate(kind, steps, probe_n, cpu: BatchExecutor, accel: BatchExecutor) ->
     return p
 
 
-def calibrate_n(kind, steps, probe_n, executors: Sequence[BatchExecutor]):
-    """N-way calibration: the same probe on every back-end, sequentially.
-    Returns (times, ok)."""
+def snap_equal_times(times: Sequence[float], spreads: Optional[Sequence[float]] = None,
+                     ok: Optional[Sequence[bool]] = None, min_rel_tol: float = 0.01) -> list[float]:
+    """hb_snap_equal_times: if the alive back-ends' times agree within
+    max(their largest measured relative spread, min_rel_tol), all of them get
+    the mean time (equal shares) — measurement noise between identical GPUs
+    must not turn into a permanent imbalance; otherwise unchanged."""
+    cnt = len(times)
+    t = np.ascontiguousarray(times, dtype=np.float64)
+    sp = np.ascontiguousarray([0.0] * cnt if spreads is None else spreads, dtype=np.float64)
+    okv = np.ascontiguousarray([1] * cnt if ok is None else [int(b) for b in ok], dtype=np.int32)
+    out = np.zeros(cnt)
+    lib.hb_snap_equal_times(_lib.ptr(t), _lib.ptr(sp), _lib.ptr(okv), cnt, float(min_rel_tol), _lib.ptr(out))
+    return [float(x) for x in out]
+
+
+def median_and_spread(samples: Sequence[float]) -> tuple[float, float]:
+    """Median of the samples and their relative range (max - min) / median."""
+    v = np.sort(np.asarray(samples, dtype=np.float64))
+    med = float(np.median(v))
+    return med, (float(v[-1] - v[0]) / med if med > 0 else 0.0)
+
+
+def calibrate_n(kind, steps, probe_n, executors: Sequence[BatchExecutor], repeats: int = 5,
+                snap_tol: Optional[float] = 0.01):
+    """N-way calibration (scheduler.cpp:30-56 over N back-ends): the same
+    probe on every back-end, sequentially, `repeats` times; a back-end's time
+    is the median of its wall_time_s, and one that throws is flagged failed
+    (time 0).  With snap_tol, times that agree within the measured spread
+    snap to equal (snap_equal_times).  Returns (times, ok).  For GPU-only
+    back-ends MultiGpuExecutor.calibrate times the probe with CUDA events on
+    every device at once."""
     if probe_n < 1:
         raise ValueError("calibrate: probe_n must be >= 1")
     req = _probe_request(kind, steps, probe_n)
-    times, ok = [], []
+    times, ok, spreads = [], [], []
     for ex in executors:
         try:
-            times.append(ex.run(req).wall_time_s)
+            med, sp = median_and_spread([ex.run(req).wall_time_s for _ in range(max(1, repeats))])
+            times.append(med)
+            spreads.append(sp)
             ok.append(True)
-        except Exception:
+        except Exception:  # noqa: BLE001 - a throwing back-end is dead (scheduler.cpp:40-49)
             times.append(0.0)
+            spreads.append(0.0)
             ok.append(False)
     if not any(ok):
         raise RuntimeError("calibrate: all back-ends failed")
+    if snap_tol is not None:
+        times = snap_equal_times(times, spreads, ok, snap_tol)
     return times, ok
 
 
@@ -118,10 +151,13 @@ def plan_allocation_n(times: Sequence[float], n_total: int,
                       ok: Optional[Sequence[bool]] = None) -> list[int]:
     """N-way peeling split (hb_plan_allocation_n): shares per back-end, in
     back-end order, summing to n_total.  For two back-ends shares ==
-    [plan.n_cpu, plan.n_accel] of plan_allocation."""
+    [plan.n_cpu, plan.n_accel] of plan_allocation.  ok = None treats a
+    non-positive or non-finite time as a failed back-end (no share)."""
     cnt = len(times)
     t = np.ascontiguousarray(times, dtype=np.float64)
-    okv = np.ascontiguousarray([1] * cnt if ok is None else [int(b) for b in ok], dtype=np.int32)
+    if ok is None:  # a non-positive / non-finite time marks a failed back-end
+        ok = [bool(np.isfinite(x) and x > 0.0) for x in t]
+    okv = np.ascontiguousarray([int(b) for b in ok], dtype=np.int32)
     shares = np.zeros(cnt, dtype=np.uint64)
     st = lib.hb_plan_allocation_n(_lib.ptr(t), _lib.ptr(okv), cnt, int(n_total), _lib.ptr(shares))
     if st != _lib.HB_OK:
@@ -236,36 +272,84 @@ def run_hybrid(plan: AllocationPlan, request: BatchRequest, cpu: BatchExecutor,
     return out
 
 
+@dataclass
+class ShardedResult:
+    merged: np.ndarray
+    walls: list            # per back-end wall of its (last) part
+    wall_s: float          # combined wall clock
+    degraded: bool = False
+    ok: list = field(default_factory=list)  # per back-end: finished its work
+
+    def __iter__(self):  # (merged, walls, wall) unpacking
+        return iter((self.merged, self.walls, self.wall_s))
+
+
 def run_sharded(shares: Sequence[int], request: BatchRequest,
-                executors: Sequence[BatchExecutor]) -> tuple[np.ndarray, list[float], float]:
+                executors: Sequence[BatchExecutor]) -> ShardedResult:
     """N-way analogue of run_hybrid (Emulated mode): contiguous slices in
-    back-end order, one host thread per back-end, merged in seed order.
-    Returns (merged results, per-back-end walls, combined wall)."""
+    back-end order, one host thread per back-end, merged in seed order.  A
+    back-end that throws anything but BatchFailure is dead for the rest of
+    the call; its slice is re-planned over the survivors (plan_allocation_n
+    with ok = False for the dead, survivors weighted by their shares) and the
+    result is flagged degraded — the N-way form of the reference's
+    re-dispatch (scheduler.cpp:162-183).  A BatchFailure is the batch's own
+    result (re-running it elsewhere reproduces it) and propagates, as does
+    the first error when every back-end has failed."""
+    from .executor import BatchFailure
     validate_request(request)
-    if sum(shares) != len(request.seeds) or len(shares) != len(executors):
+    cnt = len(executors)
+    if sum(shares) != len(request.seeds) or len(shares) != cnt:
         raise ValueError("run_sharded: shares do not match the request / executors")
     bounds = np.concatenate([[0], np.cumsum(shares)]).astype(np.int64)
-    parts: list = [None] * len(executors)
-    errs: list = [None] * len(executors)
-
-    def go(d):
-        try:
-            parts[d] = executors[d].run(BatchRequest(request.kind,
-                                                     request.seeds[bounds[d]:bounds[d + 1]],
-                                                     request.steps))
-        except Exception as e:  # noqa: BLE001
-            errs[d] = e
-
+    weights = [1.0 / s if s > 0 else 1.0 for s in shares]
+    alive = [True] * cnt
+    work = [[(int(bounds[d]), int(bounds[d + 1]))] if shares[d] > 0 else [] for d in range(cnt)]
+    parts: dict = {}
+    walls = [0.0] * cnt
+    first_err = None
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=go, args=(d,)) for d in range(len(executors)) if shares[d] > 0]
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
+    while any(work):
+        errs: list = [None] * cnt
+
+        def go(d, slices):
+            while slices:  # completed slices leave the list; the rest is orphaned on failure
+                b, e = slices[0]
+                try:
+                    r = executors[d].run(BatchRequest(request.kind, request.seeds[b:e], request.steps))
+                except Exception as ex:  # noqa: BLE001 - mirrors catch (...)
+                    errs[d] = ex
+                    return
+                parts[b] = r.results
+                walls[d] = r.wall_time_s
+                slices.pop(0)
+
+        ths = [threading.Thread(target=go, args=(d, work[d])) for d in range(cnt) if work[d]]
+        busy = [d for d in range(cnt) if work[d]]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        orphans = []
+        for d in busy:
+            if errs[d] is None:
+                work[d] = []
+                continue
+            if isinstance(errs[d], BatchFailure):
+                raise errs[d]
+            first_err = first_err or errs[d]
+            alive[d] = False
+            orphans.extend(work[d])
+            work[d] = []
+        if not orphans:
+            break
+        if not any(alive):
+            raise first_err
+        for b, e in orphans:
+            sub = plan_allocation_n(weights, e - b, alive)
+            for d in range(cnt):
+                if sub[d]:
+                    work[d].append((b, b + sub[d]))
+                b += sub[d]
     wall = time.perf_counter() - t0
-    for e in errs:
-        if e is not None:
-            raise e
-    merged = np.concatenate([p.results for p in parts if p is not None])
-    walls = [p.wall_time_s if p is not None else 0.0 for p in parts]
-    return merged, walls, wall
+    merged = np.concatenate([parts[b] for b in sorted(parts)])
+    return ShardedResult(merged, walls, wall, not all(alive), list(alive))

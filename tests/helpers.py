@@ -61,3 +61,18 @@ class FailingExecutor(hb.BatchExecutor):
 
     def run(self, request):
         raise RuntimeError("executor down")
+
+
+class NoisyStubExecutor(StubExecutor):
+    """StubExecutor whose reported wall is base x (1 + U(-noise, noise)),
+    seeded: the timing jitter of identical devices."""
+
+    def __init__(self, wall, noise=0.03, seed=0):
+        super().__init__(wall)
+        self.noise = noise
+        self.rng = np.random.default_rng(seed)
+
+    def run(self, request):
+        r = super().run(request)
+        r.wall_time_s = self.wall * (1.0 + self.rng.uniform(-self.noise, self.noise))
+        return r

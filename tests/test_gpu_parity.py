@@ -194,6 +194,56 @@ def test_multi_device_executor_single_gpu():
     assert np.array_equal(res2, res)
 
 
+@pytest.mark.parametrize("kind", [0, 1])
+def test_multi_device_degraded_redispatch(kind):
+    """Fault injection: one of four contexts is a dead device (every call
+    fails as HB_CUDA_ERROR).  Its slice is re-planned over the three
+    survivors, the merge is identical to the healthy one-device run and the
+    call is flagged degraded (scheduler.cpp:162-183, N-way); a blow-up is the
+    batch's own result and is not re-dispatched."""
+    ex = hb.MultiGpuExecutor([0, 0, 0, 0])
+    seeds = np.arange(10000, dtype=np.uint64) * np.uint64(977)
+    want = O.simulate_batch(kind, seeds, 120).results
+    ex.ctxs[2].inject_fault(hb._lib.HB_FAULT_DEVICE)
+    got = ex.run(hb.BatchRequest(kind, seeds, 120)).results
+    assert np.array_equal(got, want)
+    assert ex.last_degraded and ex.last_device_ok == [True, True, False, True]
+    ex.ctxs[0].inject_fault(hb._lib.HB_FAULT_DEVICE)  # two dead: still complete
+    ex.shares = [1000, 2000, 3000, 4000]
+    got = ex.run(hb.BatchRequest(kind, seeds, 120)).results
+    assert np.array_equal(got, want) and ex.last_device_ok == [False, True, False, True]
+    for c in ex.ctxs:
+        c.inject_fault(hb._lib.HB_FAULT_DEVICE)
+    with pytest.raises(RuntimeError):
+        ex.run(hb.BatchRequest(kind, seeds, 120))
+    for c in ex.ctxs:
+        c.inject_fault(hb._lib.HB_FAULT_NONE)
+    ex.ctxs[1].inject_fault(hb._lib.HB_FAULT_BLOWUP, int(seeds[4321]))
+    with pytest.raises(hb.BatchFailure) as e:
+        ex.run(hb.BatchRequest(kind, seeds, 120))
+    assert not ex.last_degraded
+    assert e.value.failed[0][0] == int(seeds[4321]) and len(e.value.completed) == len(seeds) - 1
+
+
+def test_calibrate_contexts_events_and_snap():
+    """hb_calibrate: a >= 5 ms probe timed with CUDA events on every context,
+    median of 5; identical devices (here: contexts on one GPU, timed
+    concurrently) snap to equal times -> equal shares; a dead device is
+    flagged and gets no share."""
+    ex = hb.MultiGpuExecutor([0, 0, 0, 0])
+    times, ok, spreads = ex.calibrate(1, 1000, 4096)
+    assert ok == [True] * 4 and all(t > 0 for t in times)
+    assert len(set(times)) == 1, (times, spreads)
+    assert hb.plan_allocation_n(times, 65536, ok) == [16384] * 4
+    ex.ctxs[3].inject_fault(hb._lib.HB_FAULT_DEVICE)
+    times, ok, _ = ex.calibrate(1, 1000, 4096)
+    assert ok == [True, True, True, False] and times[3] == 0.0
+    seeds = np.arange(5000, dtype=np.uint64)
+    assert np.array_equal(ex.run(hb.BatchRequest(1, seeds, 50)).results,
+                          O.simulate_batch(1, seeds, 50).results)
+    assert not ex.last_degraded  # the dead device had no share to lose
+
+
 def test_fp64_probe(gpu):
     ops, ms = gpu.ctx.fp64_peak()
     assert ms > 0 and 1e12 < ops < 1e14

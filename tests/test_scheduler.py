@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import paper_2502_11129_b200 as hb
-from helpers import OracleExecutor, StubExecutor
+from helpers import FailingExecutor, OracleExecutor, StubExecutor
 
 
 def profile_from(t_cpu, t_accel):
@@ -123,3 +123,31 @@ def test_run_sharded_nway():
     merged, walls, wall = hb.run_sharded(shares, req, exs)
     assert np.array_equal(merged, OracleExecutor(2).run(req).results)
     assert len(walls) == 4 and wall > 0
+
+
+def test_run_sharded_degraded_redispatch():
+    """A back-end that throws is dead: its slice is re-planned over the
+    survivors (plan_allocation_n, ok = False) and the merge is identical to a
+    healthy run, flagged degraded (scheduler.cpp:162-183, N-way)."""
+    req = request_of(1000, 20, kind=1)
+    exs = [OracleExecutor(1), FailingExecutor(), OracleExecutor(1), OracleExecutor(1)]
+    shares = hb.plan_allocation_n([1.0, 1.0, 2.0, 1.0], 1000)
+    r = hb.run_sharded(shares, req, exs)
+    assert r.degraded and r.ok == [True, False, True, True]
+    assert np.array_equal(r.merged, OracleExecutor(2).run(req).results)
+    healthy = hb.run_sharded(shares, req, [OracleExecutor(1) for _ in range(4)])
+    assert not healthy.degraded and np.array_equal(healthy.merged, r.merged)
+    with pytest.raises(RuntimeError):
+        hb.run_sharded([500, 500], request_of(1000, 20, kind=1), [FailingExecutor(), FailingExecutor()])
+
+
+def test_calibrate_n_marks_failure_and_snaps():
+    from helpers import NoisyStubExecutor
+    req_kind, steps = 1, 20
+    exs = [NoisyStubExecutor(1e-3, 0.03, seed=s) for s in range(4)] + [FailingExecutor()]
+    times, ok = hb.calibrate_n(req_kind, steps, 8, exs)
+    assert ok == [True] * 4 + [False] and times[4] == 0.0
+    assert len(set(times[:4])) == 1  # snapped to equal
+    assert hb.plan_allocation_n(times, 1000, ok) == [250, 250, 250, 250, 0]
+    t2, _ = hb.calibrate_n(req_kind, steps, 8, [StubExecutor(1.0), StubExecutor(3.0)])
+    assert t2 == [1.0, 3.0]
