@@ -508,25 +508,29 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
     """configs[4]: the full (mu + lambda) generation loop.  One bench step =
     one run_ea of `--generations` generations over `--population` genomes
     (pop + G * pop/2 variants simulated through `--sim-steps` steps each).
-    N = 1: the native device loop (hb_run_ea: device selection / variation).
-    N > 1: one rank per GPU, offspring sharded by the N-way splitter, fitness
-    all-gathered over NCCL every generation; max wall over ranks."""
+    N = 1: the native device loop (hb_run_ea on one context).
+    N > 1: rank 0 drives all N GPUs in process — hb_run_ea over N contexts:
+    offspring sharded by the throughput splitter (hb_calibrate: CUDA-event
+    probe per GPU, snapped to equal shares for equal GPUs), each GPU fed by
+    its persistent worker thread, generations chained by cross-device events
+    and the fitness slices gathered into GPU 0 by peer copies over NVLink (no
+    host synchronisation per generation for Box); the other ranks only join
+    the barrier (their time is 0, so the max over ranks is rank 0's)."""
     import torch
     import paper_2502_11129_b200 as hb
-    from paper_2502_11129_b200 import distributed as hbd
-    ex = hb.GpuExecutor(local)
     pop, G = a.population, a.generations
     evaluated = pop + G * (pop // 2)
-
-    # N > 1: the splitter's shares come from every rank timing the same probe
-    # (an offspring slice's worth of variants) on its own GPU
-    times = (hbd.calibrate_ranks(kind, a.sim_steps, max(1, (pop // 2) // ws), ex, dist)
-             if ws > 1 else None)
+    if ws > 1:
+        ex = hb.MultiGpuExecutor(list(range(ws))) if rank == 0 else None
+        calib = ex.calibrate(kind, a.sim_steps, max(1, (pop // 2) // ws)) if rank == 0 else None
+    else:
+        ex = hb.GpuExecutor(local)
+        calib = None
 
     def one():
-        if ws == 1:
-            return hb.run_ea(kind, pop, G, a.sim_steps, ex, seed=0)
-        return hbd.run_ea_sharded_device(kind, pop, G, a.sim_steps, ex, dist, seed=0, times=times)
+        if ex is None:
+            return None
+        return hb.run_ea(kind, pop, G, a.sim_steps, ex, seed=0)
 
     def max_over_ranks(x):
         if dist is None:
@@ -546,14 +550,16 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
     profs = []
     for _ in range(a.steps):
         r = one()
-        profs.append(r.profile)
+        if r is not None:
+            profs.append(r.profile)
     torch.cuda.synchronize(dev)
-    t = max_over_ranks(time.perf_counter() - t0)
+    t = max_over_ranks(time.perf_counter() - t0 if ex is not None else 0.0)
     clk = clocks.stop()
     value = evaluated * a.sim_steps * a.steps / t
     if rank == 0:
         ev = sum(p.evaluation_s for p in profs)
         tot = sum(p.total_s for p in profs)
+        host = sum(p.host_overhead_s for p in profs)
         line = {"metric": METRIC, "value": value, "unit": "variant-steps/s", "n_gpus": ws,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * t / a.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -562,27 +568,33 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
                                        f"{a.sim_steps} steps (BASELINE configs[4])",
                            "model": a.model, "population": pop, "generations": G,
                            "sim_steps": a.sim_steps, "variants_simulated_per_step": evaluated,
-                           "parallelism": f"dp{ws} offspring shards (plan_allocation_n) + "
-                                          "per-generation fitness all-gather"},
+                           "parallelism": f"{ws} GPU(s) in one process: offspring shards "
+                                          "(plan_allocation_n over hb_calibrate times), per-generation "
+                                          "fitness gather by peer copy into GPU 0",
+                           "splitter": (None if calib is None else
+                                        {"device_times_s": calib[0], "device_ok": calib[1],
+                                         "spreads": calib[2]})},
                 "e2e": {"value": value, "unit": "variant-steps/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 16 * pop,
-                        "path": "run_ea -> hb_run_ea (genomes created and selected on the device; "
-                                "final population D2H)" if ws == 1 else
-                                "run_ea_sharded_device (device-resident population on every rank; "
-                                "offspring slices evaluated per rank, NCCL fitness all-gather, "
-                                "identical device selection on every rank; final population D2H)"},
+                        "path": "run_ea -> hb_run_ea (genomes created and selected on GPU 0; "
+                                "evaluations sharded over the GPUs; final population D2H)"},
                 "evaluation_fraction": ev / tot if tot else None,
                 "phases_ms_per_run": {k: 1e3 * sum(getattr(p, k + "_s") for p in profs) / a.steps
-                                      for k in ("selection", "evaluation", "bookkeeping", "total")},
+                                      for k in ("selection", "evaluation", "bookkeeping", "total",
+                                                "host_overhead")},
+                "host_overhead_us_per_generation": 1e6 * host / max(1, len(profs)) / (G + 1),
                 "best_fitness": r.best_fitness, "clocks": clk,
-                # per run: genome init; per evaluation the simulation (+ the
-                # fitness gather, except Box, whose kernel writes fitness);
-                # per generation the selection (cluster sort, then tie fix +
+                # per run: genome init; per evaluation and GPU the simulation
+                # (+ the fitness gather, except Box, whose kernel writes
+                # fitness; + the state initialiser for multi-body models); per
+                # generation the selection (cluster sort, then tie fix +
                 # select + offspring in one kernel)
-                "gpu_launches": a.steps * (1 + (1 if int(kind) == 0 else 2) * (G + 1) + 2 * G),
+                "gpu_launches": a.steps * (1 + (1 if int(kind) == 0 else 3) * (G + 1) * ws + 2 * G),
                 "parity": "genomes + fitness bit-identical to reference run_ea"}
         print(json.dumps(line))
-    ex.ctx.close()
+    if ex is not None:
+        for c in (ex.ctxs if ws > 1 else [ex.ctx]):
+            c.close()
     if dist is not None:
         dist.destroy_process_group()
 

@@ -130,6 +130,24 @@ hb_status hb_ctx_set_precision(hb_ctx* ctx, int precision);
  * on the call's critical path.  0 disables it (always stage + DMA). */
 hb_status hb_ctx_set_zero_copy(hb_ctx* ctx, int enable);
 
+/* ---- utilisation trace (BatchResult::utilization_trace, executor.hpp:26-35)
+ * With the monitor on, every hb_run_batch on this context records a trace:
+ * NVML GPU utilisation (nvmlDeviceGetUtilizationRates, the driver's
+ * libnvidia-ml.so.1 loaded at run time; absent NVML = no such samples) at
+ * 20 Hz while the call runs, t in seconds since the call started, then one
+ * final synchronised sample at t = the call's wall time: the share of the
+ * wall time during which the stepping kernel ran (CUDA events around the
+ * launch) — the quantity NVML reports, exact for this call however short.
+ * Off by default (it adds two event records and a sampler hand-off). */
+typedef struct {
+    double t;             /* seconds since the call started */
+    double accel_percent; /* [0, 100] */
+} hb_util_sample;
+hb_status hb_ctx_set_monitor(hb_ctx* ctx, int enable);
+/* Samples of the last monitored hb_run_batch: *count = their number; the
+ * first min(cap, *count) are copied to out (nullable). */
+hb_status hb_last_utilization(const hb_ctx* ctx, hb_util_sample* out, size_t cap, size_t* count);
+
 /* Fault injection (test seam; the counterpart of the reference's
  * simulate_fn seam, executor.hpp:89-90, that its tests use to make a back-end
  * throw).  Applies to hb_run_batch calls on this context until reset:
@@ -295,6 +313,11 @@ typedef struct {
     double evaluation_s;
     double bookkeeping_s;
     double total_s;
+    /* wall time of the call not covered by device work (first launch
+     * latency, enqueue stalls, host round trips, final sync and copies):
+     * total_s minus the device span of the loop, where a device span was
+     * measured (the queued loops), else 0 */
+    double host_overhead_s;
 } hb_phase_profile;
 
 hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, int kind, size_t pop,

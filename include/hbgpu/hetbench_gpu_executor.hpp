@@ -33,9 +33,19 @@ static_assert(sizeof(hb_variant_result) == sizeof(hetbench::VariantResult),
 
 class gpu_executor : public hetbench::batch_executor {
 public:
-    explicit gpu_executor(int device = 0) {
+    // monitor: fill BatchResult::utilization_trace (hb_ctx_set_monitor: NVML
+    // samples while the call runs + the call's kernel-busy share), as
+    // cpu_executor(workers, monitor = true) fills its CPU trace
+    // (executor.hpp:78-80); the sweep's accel_util_mean comes from it
+    // (sweep.cpp:119).
+    explicit gpu_executor(int device = 0, bool monitor = true) {
         if (hb_ctx_create(device, &ctx_) != HB_OK)
             throw std::runtime_error(std::string("gpu_executor: ") + hb_global_error());
+        if (monitor && hb_ctx_set_monitor(ctx_, 1) != HB_OK) {
+            hb_ctx_destroy(ctx_);
+            throw std::runtime_error(std::string("gpu_executor: ") + hb_global_error());
+        }
+        monitor_ = monitor;
     }
     ~gpu_executor() override { hb_ctx_destroy(ctx_); }
     gpu_executor(const gpu_executor&) = delete;
@@ -69,6 +79,13 @@ public:
         }
         if (st != HB_OK) throw std::runtime_error(std::string("gpu_executor: ") + hb_last_error(ctx_));
         out.wall_time_s = wall;
+        if (monitor_) {
+            std::size_t count = 0;
+            hb_last_utilization(ctx_, nullptr, 0, &count);
+            std::vector<hb_util_sample> tr(count);
+            hb_last_utilization(ctx_, tr.data(), tr.size(), &count);
+            for (const hb_util_sample& u : tr) out.utilization_trace.push_back({u.t, u.accel_percent});
+        }
         return out;
     }
 
@@ -77,6 +94,7 @@ public:
 
 private:
     hb_ctx* ctx_ = nullptr;
+    bool monitor_ = true;
 };
 
 }  // namespace hbgpu

@@ -27,6 +27,8 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvml.h>
 
 #include "hb_internal.h"
 #include "hb_model.h"
@@ -230,6 +232,97 @@ private:
     std::thread th_;
 };
 
+// ---------------------------------------------------------------------------
+// NVML utilisation sampler (the accelerator side of the reference's
+// UtilSampler, monitor.hpp:78-94, whose accel_percent is always 0,
+// monitor.cpp:164,177).  NVML is loaded with dlopen (the driver's
+// libnvidia-ml.so.1): no link-time dependency, and without NVML the trace
+// holds only the final synchronised sample.  One persistent thread per
+// context samples nvmlDeviceGetUtilizationRates at 20 Hz while a call is
+// running.
+struct Nvml {
+    using init_t = nvmlReturn_t (*)();
+    using by_pci_t = nvmlReturn_t (*)(const char*, nvmlDevice_t*);
+    using util_t = nvmlReturn_t (*)(nvmlDevice_t, nvmlUtilization_t*);
+    init_t init = nullptr;
+    by_pci_t by_pci = nullptr;
+    util_t util = nullptr;
+    bool ok = false;
+    static const Nvml& get() {
+        static Nvml n = [] {
+            Nvml x;
+            void* h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+            if (!h) return x;
+            x.init = reinterpret_cast<init_t>(dlsym(h, "nvmlInit_v2"));
+            x.by_pci = reinterpret_cast<by_pci_t>(dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2"));
+            x.util = reinterpret_cast<util_t>(dlsym(h, "nvmlDeviceGetUtilizationRates"));
+            x.ok = x.init && x.by_pci && x.util && x.init() == NVML_SUCCESS;
+            return x;
+        }();
+        return n;
+    }
+};
+
+class UtilMonitor {
+public:
+    explicit UtilMonitor(int device) {
+        const Nvml& nv = Nvml::get();
+        char bus[32] = {0};
+        if (nv.ok && cudaDeviceGetPCIBusId(bus, sizeof bus, device) == cudaSuccess &&
+            nv.by_pci(bus, &dev_) == NVML_SUCCESS)
+            have_ = true;
+        cudaGetLastError();
+        if (have_) th_ = std::thread([this] { loop(); });
+    }
+    ~UtilMonitor() {
+        {
+            std::lock_guard<std::mutex> g(m_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        if (th_.joinable()) th_.join();
+    }
+    void start() {
+        std::lock_guard<std::mutex> g(m_);
+        trace_.clear();
+        t0_ = std::chrono::steady_clock::now();
+        running_ = true;
+        cv_.notify_all();
+    }
+    // stops sampling; appends the final synchronised sample
+    std::vector<hb_util_sample> stop(double final_t, double final_percent) {
+        std::unique_lock<std::mutex> lk(m_);
+        running_ = false;
+        trace_.push_back(hb_util_sample{final_t, final_percent});
+        return trace_;
+    }
+
+private:
+    void loop() {
+        std::unique_lock<std::mutex> lk(m_);
+        for (;;) {
+            cv_.wait(lk, [&] { return stop_ || running_; });
+            if (stop_) return;
+            while (running_ && !stop_) {
+                if (cv_.wait_for(lk, std::chrono::milliseconds(50), [&] { return stop_ || !running_; })) break;
+                nvmlUtilization_t u{};
+                if (Nvml::get().util(dev_, &u) == NVML_SUCCESS) {
+                    const double t = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0_).count();
+                    trace_.push_back(hb_util_sample{t, static_cast<double>(std::min(100u, u.gpu))});
+                }
+            }
+        }
+    }
+    nvmlDevice_t dev_{};
+    bool have_ = false;
+    std::mutex m_;
+    std::condition_variable cv_;
+    bool running_ = false, stop_ = false;
+    std::chrono::steady_clock::time_point t0_;
+    std::vector<hb_util_sample> trace_;
+    std::thread th_;
+};
+
 int default_host_threads() {
     unsigned hc = std::thread::hardware_concurrency();
     return static_cast<int>(std::min(64u, std::max(1u, hc)));
@@ -410,6 +503,7 @@ struct hb_ctx {
     double* h_ea_fit = nullptr;
     cudaEvent_t ea_ev[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ea_timing;  // per-generation selection brackets of the queued loop
+    std::vector<cudaEvent_t> ea_chain;   // multi-context loop: per-generation hand-over events
     cudaStream_t ea_copy = nullptr;      // final-population D2H overlapping the last evaluation
     cudaEvent_t ea_sel_done = nullptr;
     cudaGraphExec_t ea_graph[2] = {nullptr, nullptr};  // select/vary cur -> cur ^ 1, for d_ea_pop_cap
@@ -437,6 +531,11 @@ struct hb_ctx {
     size_t last_n = 0;
     bool counters_dirty = true;  // device counters need a reset before the next launch
     bool zero_copy = true;       // Box: read seeds / write results through host mappings
+    // utilisation trace of hb_run_batch (hb_ctx_set_monitor)
+    UtilMonitor* monitor = nullptr;
+    cudaEvent_t mon_ev[2] = {nullptr, nullptr};  // kernel bracket of the call
+    bool mon_armed = false;                       // mon_ev recorded by this call
+    std::vector<hb_util_sample> util_trace;
     int fault_mode = HB_FAULT_NONE;  // hb_ctx_inject_fault (test seam)
     uint64_t fault_seed = 0;
 
@@ -499,7 +598,8 @@ hb_status ensure_capacity(hb_ctx* c, int kind, size_t n, bool need_init) {
         cudaFreeHost(c->h_seeds); cudaFreeHost(c->h_out); cudaFreeHost(c->h_fail);
         c->h_seeds = nullptr; c->h_out = nullptr; c->h_fail = nullptr;
         const size_t cap = std::max(n, c->h_n_cap * 2);
-        HB_TRY(c->cuda(cudaHostAlloc(&c->h_seeds, cap * sizeof(uint64_t), 0), "cudaHostAlloc(seeds)"));
+        HB_TRY(c->cuda(cudaHostAlloc(&c->h_seeds, cap * sizeof(uint64_t), cudaHostAllocPortable),
+                       "cudaHostAlloc(seeds)"));
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_out, cap * sizeof(hb_variant_result), 0), "cudaHostAlloc(out)"));
         HB_TRY(c->cuda(cudaHostAlloc(&c->h_fail, cap * sizeof(uint64_t), 0), "cudaHostAlloc(fail)"));
         c->h_n_cap = cap;
@@ -638,12 +738,22 @@ hb_status stage_inputs(hb_ctx* c, int kind, const uint64_t* seeds, size_t n) {
     return HB_OK;
 }
 
-// One stepping launch of this context's kernel family / precision.
-cudaError_t launch_kernel(hb_ctx* c, int kind, const hb::SimArgs& a) {
+cudaError_t launch_kernel_raw(hb_ctx* c, int kind, const hb::SimArgs& a) {
     if (fp32_for(c, kind)) return hb::launch_sim_fp32(kind, a, c->stream);
     if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO)
         return hb::launch_box_graph(c->box_graph, a, c->stream, c->sms);
     return hb::launch_sim(kind, a, c->stream, c->sms, c->kernel_variant);
+}
+
+// One stepping launch of this context's kernel family / precision; with the
+// monitor on, bracketed by CUDA events (the final utilisation sample).
+cudaError_t launch_kernel(hb_ctx* c, int kind, const hb::SimArgs& a) {
+    if (!c->monitor) return launch_kernel_raw(c, kind, a);
+    cudaError_t e = cudaEventRecord(c->mon_ev[0], c->stream);
+    if (e == cudaSuccess) e = launch_kernel_raw(c, kind, a);
+    if (e == cudaSuccess) e = cudaEventRecord(c->mon_ev[1], c->stream);
+    c->mon_armed = e == cudaSuccess;
+    return e;
 }
 
 hb_status launch(hb_ctx* c, int kind, size_t n, uint64_t steps, double dt, bool from_seeds,
@@ -770,6 +880,8 @@ hb_status hb_ctx_create(int device, hb_ctx** out) {
 void hb_ctx_destroy(hb_ctx* c) {
     if (!c) return;
     delete c->worker;
+    delete c->monitor;
+    for (cudaEvent_t e : c->mon_ev) if (e) cudaEventDestroy(e);
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     cudaFree(c->d_init); cudaFree(c->d_trig); cudaFree(c->d_seeds); cudaFree(c->d_out); cudaFree(c->d_fail);
@@ -781,6 +893,7 @@ void hb_ctx_destroy(hb_ctx* c) {
     cudaFreeHost(c->h_ea_gen); cudaFreeHost(c->h_ea_fit);
     for (cudaEvent_t e : c->ea_ev) if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ea_timing) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ea_chain) cudaEventDestroy(e);
     if (c->ea_sel_done) cudaEventDestroy(c->ea_sel_done);
     if (c->ea_copy) cudaStreamDestroy(c->ea_copy);
     for (cudaGraphExec_t g : c->ea_graph) if (g) cudaGraphExecDestroy(g);
@@ -936,9 +1049,37 @@ static void apply_blowup_fault(hb_ctx* c, const uint64_t* seeds, size_t n, hb_va
     *any = true;
 }
 
+static hb_status run_batch_impl(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
+                                hb_variant_result* out, uint64_t* fail_step, double* wall_time_s,
+                                std::chrono::steady_clock::time_point t0);
+
+// The drop-in call.  With the monitor on (hb_ctx_set_monitor) the call is
+// sampled by the context's NVML thread and closed by one synchronised
+// sample: the share of the call's wall time the stepping kernel ran
+// (CUDA events around the launch) — NVML's "percent of time a kernel was
+// executing", exact for this call.
 hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
                        hb_variant_result* out, uint64_t* fail_step, double* wall_time_s) {
     const auto t0 = std::chrono::steady_clock::now();
+    if (!c || !c->monitor) return run_batch_impl(c, kind, seeds, n, steps, out, fail_step, wall_time_s, t0);
+    c->monitor->start();
+    c->mon_armed = false;
+    double wall = 0.0;
+    const hb_status st = run_batch_impl(c, kind, seeds, n, steps, out, fail_step, &wall, t0);
+    if (wall_time_s) *wall_time_s = wall;
+    double busy = 0.0;
+    float ms = 0.f;
+    if (c->mon_armed && cudaEventSynchronize(c->mon_ev[1]) == cudaSuccess &&
+        cudaEventElapsedTime(&ms, c->mon_ev[0], c->mon_ev[1]) == cudaSuccess && wall > 0.0)
+        busy = std::min(100.0, 100.0 * 1e-3 * ms / wall);
+    cudaGetLastError();
+    c->util_trace = c->monitor->stop(wall, busy);
+    return st;
+}
+
+static hb_status run_batch_impl(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uint64_t steps,
+                                hb_variant_result* out, uint64_t* fail_step, double* wall_time_s,
+                                std::chrono::steady_clock::time_point t0) {
     HB_TRY(validate(c, kind, seeds, n, steps, out));
     if (c->fault_mode == HB_FAULT_DEVICE)
         return c->fail(HB_CUDA_ERROR, "injected device fault (hb_ctx_inject_fault)");
@@ -964,6 +1105,30 @@ hb_status hb_run_batch(hb_ctx* c, int kind, const uint64_t* seeds, size_t n, uin
     apply_blowup_fault(c, seeds, n, out, fail_step, &any);
     if (wall_time_s) *wall_time_s = std::max(elapsed_s(t0), 1e-9);
     if (any) return c->fail(HB_BLOWUP_PARTIAL, "numerical blow-up in batch");
+    return HB_OK;
+}
+
+hb_status hb_ctx_set_monitor(hb_ctx* c, int enable) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (!enable) {
+        delete c->monitor;
+        c->monitor = nullptr;
+        c->util_trace.clear();
+        return HB_OK;
+    }
+    if (c->monitor) return HB_OK;
+    HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+    for (cudaEvent_t& e : c->mon_ev)
+        if (!e) HB_TRY(c->cuda(cudaEventCreate(&e), "event"));
+    c->monitor = new UtilMonitor(c->device);
+    return HB_OK;
+}
+
+hb_status hb_last_utilization(const hb_ctx* c, hb_util_sample* out, size_t cap, size_t* count) {
+    if (!c || !count) return set_global(HB_INVALID_ARG, "bad arguments");
+    *count = c->util_trace.size();
+    if (out)
+        for (size_t i = 0; i < std::min(cap, c->util_trace.size()); ++i) out[i] = c->util_trace[i];
     return HB_OK;
 }
 
@@ -1435,6 +1600,24 @@ double fold_max(double init, const double* f, size_t n) {
     return init;
 }
 
+// The stepping launch of an evaluation (+ the fitness gather): the initial
+// state is built from the seeds on the device (Box) or already in c->d_init.
+hb_status eval_kernel(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uint64_t steps,
+                      double* d_fitness) {
+    const bool dev_init = init_on_device(c, kind);
+    if (c->counters_dirty) {
+        HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
+        c->counters_dirty = false;
+    }
+    hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
+                  c->d_out, c->d_fail, c->d_count, nullptr, nullptr, c->d_ops};
+    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO) a.fitness = d_fitness;  // no records, no gather
+    HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
+    if (!a.fitness)
+        HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
+    return HB_OK;
+}
+
 // Launch the simulation of n device-resident seeds on c's device; fitness
 // lands in d_fitness (c's device).  Models initialised on the host take the
 // seeds through the host initialiser first (blocking).  Counters are read
@@ -1467,16 +1650,7 @@ hb_status eval_start(hb_ctx* c, int kind, const uint64_t* d_seeds, size_t n, uin
         }
         tr.mark("h2d_enqueue");
     }
-    if (c->counters_dirty) {
-        HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
-        c->counters_dirty = false;
-    }
-    hb::SimArgs a{dev_init ? nullptr : c->d_init, d_seeds, n, n, steps, hb::kSimDt,
-                  c->d_out, c->d_fail, c->d_count, nullptr, nullptr, c->d_ops};
-    if (kind == hb::Box && c->kernel_variant == HB_KERNEL_AUTO) a.fitness = d_fitness;  // no records, no gather
-    HB_TRY(c->cuda(launch_kernel(c, kind, a), "kernel launch"));
-    if (!a.fitness)
-        HB_TRY(c->cuda(hb::ea_fitness_from_results(c->d_out, n, d_fitness, c->stream), "fitness gather"));
+    HB_TRY(eval_kernel(c, kind, d_seeds, n, steps, d_fitness));
     if (read_counts)
         HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
                                        c->stream), "D2H count"));
@@ -1519,13 +1693,14 @@ hb_status eval_sharded(hb_ctx* const* ctxs, int count, const std::vector<uint64_
     }
     std::vector<hb_status> st(count, HB_OK);
     std::vector<std::string> err(count);
-    std::vector<std::thread> th;
+    std::vector<int> busy;
     size_t begin = 0;
     for (int d = 0; d < count; ++d) {
         const size_t b = begin, len = shares[d];
         begin += len;
         if (len == 0) continue;
-        th.emplace_back([&, d, b, len] {
+        busy.push_back(d);
+        worker_of(ctxs[d]).submit([&, d, b, len] {
             hb_ctx* c = ctxs[d];
             auto run = [&]() -> hb_status {
                 HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
@@ -1547,9 +1722,250 @@ hb_status eval_sharded(hb_ctx* const* ctxs, int count, const std::vector<uint64_
             if (st[d] != HB_OK) err[d] = c->err;
         });
     }
-    for (auto& t : th) t.join();
+    for (int d : busy) worker_of(ctxs[d]).wait();
     for (int d = 0; d < count; ++d)
         if (st[d] != HB_OK) return ctxs[0]->fail(st[d], err[d]);
+    return HB_OK;
+}
+
+// Spin (briefly), then yield, until `a` reaches `v`: host-side ordering of
+// the enqueues of the queued multi-context loop (a stream may only wait on an
+// event after the event's record has been enqueued).
+void wait_at_least(const std::atomic<uint64_t>& a, uint64_t v) {
+    for (int i = 0; a.load(std::memory_order_acquire) < v; ++i)
+        if (i > 2000) std::this_thread::yield();
+}
+
+hb_status ensure_events(hb_ctx* c, std::vector<cudaEvent_t>& ev, size_t n, unsigned flags) {
+    while (ev.size() < n) {
+        cudaEvent_t e;
+        HB_TRY(c->cuda(cudaEventCreateWithFlags(&e, flags), "event"));
+        ev.push_back(e);
+    }
+    return HB_OK;
+}
+
+// The generation loop over `count` contexts, queued: no host synchronisation
+// per generation for device-initialised models (Box) and exactly one (the
+// offspring seeds for the host's libm cos / sin) for the others.  Device 0
+// holds the population and runs the selection graph; every device d
+// evaluates its contiguous slice of each evaluation (shares from the
+// splitter) on its own stream, driven by its persistent worker thread:
+//   dev d: wait(sel[g]) -> seeds slice in (peer copy) -> [init] -> kernel ->
+//          fitness slice out (peer copy into device 0's population) -> done[d][g]
+//   dev 0: wait(done[*][g-1]) -> selection graph -> sel[g] -> own slice
+// The host threads only order their enqueues (an event must be recorded
+// before a stream waits on it); all data dependencies are stream / event
+// ordered on the devices.  Failure counters accumulate over the loop and are
+// read once at the end: *any_fail tells the caller to re-run checked.
+hb_status run_ea_queued(hb_ctx* const* ctxs, int count, int kind, size_t pop, uint64_t G, uint64_t steps,
+                        uint64_t seed, const std::vector<uint64_t>& sh_pop, const std::vector<uint64_t>& sh_mu,
+                        uint64_t* const d_gen[2], double* const d_fit[2], uint64_t* genomes_out,
+                        double* fitness_out, double* best_out, hb_phase_profile* prof_out, bool* any_fail) {
+    using clk = std::chrono::steady_clock;
+    const auto t_start = clk::now();
+    hb_ctx* c0 = ctxs[0];
+    const size_t mu = pop / 2;
+    const bool dev_init = init_on_device(c0, kind);
+    const int J2 = 2 * hb::init_angles(kind);  // trig rows (host-initialised kinds)
+    // slices: evaluation g covers [off_g, off_g + n_g) of buffer g & 1
+    std::vector<std::vector<size_t>> beg(2, std::vector<size_t>(count + 1, 0));
+    for (int d = 0; d < count; ++d) {
+        beg[0][d + 1] = beg[0][d] + sh_pop[d];
+        beg[1][d + 1] = beg[1][d] + sh_mu[d];
+    }
+    auto n_of = [&](uint64_t g) { return g == 0 ? pop : mu; };
+    auto off_of = [&](uint64_t g) { return g == 0 ? size_t{0} : mu; };
+    auto b_of = [&](uint64_t g, int d) { return beg[g == 0 ? 0 : 1][d]; };
+    auto len_of = [&](uint64_t g, int d) { return g == 0 ? sh_pop[d] : sh_mu[d]; };
+
+    // capacities and events (synchronous allocations happen here, up front)
+    for (int d = 0; d < count; ++d) {
+        hb_ctx* c = ctxs[d];
+        const size_t cap = std::max<size_t>(std::max(sh_pop[d], sh_mu[d]), d == 0 && !dev_init ? pop : 1);
+        HB_TRY(ensure_capacity(c, kind, cap, !dev_init));
+        HB_TRY(grow_dev(c, &c->d_ea_fit, c->d_ea_fit_cap, cap, "cudaMalloc(ea fit)"));
+        HB_TRY(ensure_events(c, c->ea_chain, G + 1, cudaEventDisableTiming));
+        if (c->counters_dirty) {
+            HB_TRY(c->cuda(cudaMemsetAsync(c->d_count, 0, 2 * sizeof(unsigned), c->stream), "memset(count)"));
+            c->counters_dirty = false;
+        }
+    }
+    HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
+    HB_TRY(ensure_events(c0, c0->ea_timing, 2 * G + 2, cudaEventDefault));
+    if (!c0->ea_copy) {
+        HB_TRY(c0->cuda(cudaStreamCreateWithFlags(&c0->ea_copy, cudaStreamNonBlocking), "stream"));
+        HB_TRY(c0->cuda(cudaEventCreateWithFlags(&c0->ea_sel_done, cudaEventDisableTiming), "event"));
+    }
+    cudaEvent_t* tev = c0->ea_timing.data();
+    cudaEvent_t* sel = c0->ea_chain.data();  // sel[g]: population g is ready on device 0
+
+    std::atomic<uint64_t> posted{0};  // sel[g] (Box) / host trig rows of g (others) recorded for g < posted
+    std::vector<std::atomic<uint64_t>> done(count);
+    for (auto& x : done) x.store(0);
+    std::atomic<int> abort{0};
+    std::vector<hb_status> st(count, HB_OK);
+    std::vector<std::string> err(count);
+
+    // one evaluation slice on context c (d >= 1: through c's own buffers)
+    auto slice = [&](int d, uint64_t g) -> hb_status {
+        hb_ctx* c = ctxs[d];
+        const size_t n = n_of(g), b = b_of(g, d), len = len_of(g, d);
+        uint64_t* src = d_gen[g & 1] + off_of(g) + b;
+        double* dst = d_fit[g & 1] + off_of(g) + b;
+        if (len == 0) return HB_OK;
+        const uint64_t* seeds = src;
+        if (!dev_init) {  // seeds and cos / sin rows from device 0's pinned staging
+            HB_TRY(c->cuda(cudaMemcpyAsync(c->d_seeds, c0->h_seeds + b, len * sizeof(uint64_t),
+                                           cudaMemcpyHostToDevice, c->stream), "H2D seeds"));
+            HB_TRY(c->cuda(cudaMemcpy2DAsync(c->d_trig, len * sizeof(double), c0->h_init + b, n * sizeof(double),
+                                             len * sizeof(double), J2, cudaMemcpyHostToDevice, c->stream),
+                           "H2D trig"));
+            HB_TRY(c->cuda(hb::launch_init(kind, c->d_seeds, c->d_trig, len, c->d_init, c->stream), "init kernel"));
+            seeds = c->d_seeds;
+        } else if (d > 0) {
+            HB_TRY(c->cuda(cudaMemcpyPeerAsync(c->d_seeds, c->device, src, c0->device, len * sizeof(uint64_t),
+                                               c->stream), "peer seeds"));
+            seeds = c->d_seeds;
+        }
+        if (d == 0) return eval_kernel(c, kind, seeds, len, steps, dst);
+        HB_TRY(eval_kernel(c, kind, seeds, len, steps, c->d_ea_fit));
+        return c->cuda(cudaMemcpyPeerAsync(dst, c0->device, c->d_ea_fit, c->device, len * sizeof(double),
+                                           c->stream), "peer fitness");
+    };
+    for (int d = 1; d < count; ++d) {
+        if (sh_pop[d] == 0 && sh_mu[d] == 0) {
+            done[d].store(G + 1);
+            continue;
+        }
+        worker_of(ctxs[d]).submit([&, d] {
+            hb_ctx* c = ctxs[d];
+            auto run = [&]() -> hb_status {
+                HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+                for (uint64_t g = 0; g <= G; ++g) {
+                    wait_at_least(posted, g + 1);
+                    if (abort.load()) return HB_OK;
+                    if (dev_init) HB_TRY(c->cuda(cudaStreamWaitEvent(c->stream, sel[g], 0), "wait"));
+                    HB_TRY(slice(d, g));
+                    HB_TRY(c->cuda(cudaEventRecord(c->ea_chain[g], c->stream), "record"));
+                    done[d].store(g + 1, std::memory_order_release);
+                }
+                return HB_OK;
+            };
+            st[d] = run();
+            if (st[d] != HB_OK) {
+                err[d] = c->err;
+                abort.store(1);
+                done[d].store(G + 1);
+            }
+        });
+    }
+    // device 0 (this thread)
+    auto host_rows = [&](uint64_t g) -> hb_status {  // offspring seeds to the host, libm cos / sin rows
+        const size_t n = n_of(g);
+        HB_TRY(c0->cuda(cudaMemcpyAsync(c0->h_seeds, d_gen[g & 1] + off_of(g), n * sizeof(uint64_t),
+                                        cudaMemcpyDeviceToHost, c0->stream), "D2H seeds"));
+        HB_TRY(c0->cuda(cudaStreamSynchronize(c0->stream), "stream sync"));
+        const uint64_t* hs = c0->h_seeds;
+        double* trig = c0->h_init;
+        pool_of(c0).run(n, [&](size_t b, size_t e) { trig_range(kind, hs, b, e, trig, n); }, 64);
+        return HB_OK;
+    };
+    auto main_loop = [&]() -> hb_status {
+        HB_TRY(c0->cuda(cudaEventRecord(tev[0], c0->stream), "record"));
+        HB_TRY(c0->cuda(hb::ea_init_genomes(seed, pop, d_gen[0], c0->stream, c0->d_ea_g), "init genomes"));
+        for (uint64_t g = 0; g <= G; ++g) {
+            if (g > 0) {
+                for (int d = 1; d < count; ++d) {
+                    if (len_of(g - 1, d) == 0) continue;
+                    wait_at_least(done[d], g);
+                    if (abort.load()) return HB_OK;
+                    HB_TRY(c0->cuda(cudaStreamWaitEvent(c0->stream, ctxs[d]->ea_chain[g - 1], 0), "wait"));
+                }
+                HB_TRY(c0->cuda(cudaEventRecord(tev[2 * g], c0->stream), "record"));
+                HB_TRY(c0->cuda(cudaGraphLaunch(c0->ea_graph[(g - 1) & 1], c0->stream), "select/vary"));
+                HB_TRY(c0->cuda(cudaEventRecord(tev[2 * g + 1], c0->stream), "record"));
+                if (g == G) {  // final genomes + parent fitness out while the offspring evaluate
+                    const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
+                    HB_TRY(c0->cuda(cudaEventRecord(c0->ea_sel_done, c0->stream), "record"));
+                    HB_TRY(c0->cuda(cudaStreamWaitEvent(c0->ea_copy, c0->ea_sel_done, 0), "wait"));
+                    HB_TRY(c0->cuda(cudaMemcpyAsync(pg ? genomes_out : c0->h_ea_gen, d_gen[G & 1],
+                                                    pop * sizeof(uint64_t), cudaMemcpyDeviceToHost, c0->ea_copy),
+                                    "D2H"));
+                    HB_TRY(c0->cuda(cudaMemcpyAsync(pf ? fitness_out : c0->h_ea_fit, d_fit[G & 1],
+                                                    mu * sizeof(double), cudaMemcpyDeviceToHost, c0->ea_copy),
+                                    "D2H"));
+                }
+            }
+            if (!dev_init) HB_TRY(host_rows(g));
+            HB_TRY(c0->cuda(cudaEventRecord(sel[g], c0->stream), "record"));
+            posted.store(g + 1, std::memory_order_release);
+            HB_TRY(slice(0, g));
+        }
+        for (int d = 1; d < count; ++d) {
+            if (len_of(G, d) == 0) continue;
+            wait_at_least(done[d], G + 1);
+            if (abort.load()) return HB_OK;
+            HB_TRY(c0->cuda(cudaStreamWaitEvent(c0->stream, ctxs[d]->ea_chain[G], 0), "wait"));
+        }
+        return c0->cuda(cudaEventRecord(tev[1], c0->stream), "record");
+    };
+    hb_status st0 = main_loop();
+    if (st0 != HB_OK) {
+        abort.store(1);
+        posted.store(G + 2);
+    }
+    for (int d = 1; d < count; ++d)
+        if (sh_pop[d] || sh_mu[d]) worker_of(ctxs[d]).wait();
+    const auto t_enq = clk::now();
+    if (st0 != HB_OK) return st0;
+    for (int d = 1; d < count; ++d)
+        if (st[d] != HB_OK) return c0->fail(st[d], "device " + std::to_string(d) + ": " + err[d]);
+    // results: offspring fitness of the last generation, then every device's
+    // accumulated failure counter
+    const bool pg = is_pinned(genomes_out), pf = is_pinned(fitness_out);
+    double* h_fit = pf ? fitness_out : c0->h_ea_fit;
+    HB_TRY(c0->cuda(cudaMemcpyAsync(h_fit + mu, d_fit[G & 1] + mu, mu * sizeof(double), cudaMemcpyDeviceToHost,
+                                    c0->stream), "D2H"));
+    uint64_t failed = 0;
+    for (int d = 0; d < count; ++d) {
+        hb_ctx* c = ctxs[d];
+        HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+        HB_TRY(c->cuda(cudaMemcpyAsync(c->h_count, c->d_count, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                       c->stream), "D2H count"));
+    }
+    for (int d = 0; d < count; ++d) {
+        hb_ctx* c = ctxs[d];
+        HB_TRY(c->cuda(cudaSetDevice(c->device), "cudaSetDevice"));
+        HB_TRY(c->cuda(cudaStreamSynchronize(c->stream), "sync"));
+        c->last_failed = c->h_count[0];
+        c->last_replays = c->h_count[1];
+        c->counters_dirty = (c->h_count[0] | c->h_count[1]) != 0;
+        failed += c->h_count[0];
+    }
+    HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
+    HB_TRY(c0->cuda(cudaStreamSynchronize(c0->ea_copy), "sync"));
+    *any_fail = failed != 0;
+    if (*any_fail) return HB_OK;
+    if (!pg) std::memcpy(genomes_out, c0->h_ea_gen, pop * sizeof(uint64_t));
+    if (!pf) std::memcpy(fitness_out, c0->h_ea_fit, pop * sizeof(double));
+    if (best_out) *best_out = fold_max(fitness_out[0], fitness_out + mu, mu);
+    hb_phase_profile prof{};
+    float ms = 0.f;
+    double sel_s = 0.0;
+    for (uint64_t g = 1; g <= G; ++g) {
+        cudaEventElapsedTime(&ms, tev[2 * g], tev[2 * g + 1]);
+        sel_s += 1e-3 * ms;
+    }
+    cudaEventElapsedTime(&ms, tev[0], tev[1]);
+    const double span = 1e-3 * ms;
+    prof.total_s = elapsed_s(t_start);
+    prof.selection_s = std::min(sel_s, prof.total_s);
+    prof.evaluation_s = std::min(std::max(span - sel_s, 0.0), prof.total_s - prof.selection_s);
+    prof.bookkeeping_s = prof.total_s - prof.selection_s - prof.evaluation_s;
+    prof.host_overhead_s = std::max(0.0, prof.total_s - span);
+    (void)t_enq;
+    *prof_out = prof;
     return HB_OK;
 }
 
@@ -1763,9 +2179,34 @@ hb_status hb_run_ea(hb_ctx* const* ctxs, int count, const double* device_times, 
             prof.selection_s = std::min(sel, prof.total_s);
             prof.evaluation_s = std::min(std::max(1e-3 * ms - sel, 0.0), prof.total_s - prof.selection_s);
             prof.bookkeeping_s = prof.total_s - prof.selection_s - prof.evaluation_s;
+            prof.host_overhead_s = std::max(0.0, prof.total_s - 1e-3 * ms);
             if (profile) *profile = prof;
             return HB_OK;
         }
+    }
+
+    // Several contexts (or a host-initialised model): the queued
+    // multi-context loop — persistent per-device workers, event-chained
+    // generations, one host round trip per generation only for the libm
+    // cos / sin of multi-body offspring.  A blow-up anywhere falls through to
+    // the checked loop below, which reports it exactly.
+    bool uniform = true;
+    for (int d = 0; d < count; ++d)
+        uniform = uniform && ctxs[d] && ctxs[d]->kernel_variant == c0->kernel_variant &&
+                  ctxs[d]->precision == c0->precision;
+    if (uniform && !history_genomes && !history_fitness && !(count == 1 && init_on_device(c0, kind)) &&
+        (init_on_device(c0, kind) || trig_init(c0, kind))) {
+        bool any = false;
+        hb_phase_profile qp{};
+        HB_TRY(run_ea_queued(ctxs, count, kind, pop, generations, steps, seed, shares_for(pop), shares_for(mu),
+                             d_gen, d_fit, genomes_out, fitness_out, best_out, &qp, &any));
+        if (!any) {
+            qp.total_s = elapsed_s(t_start);
+            qp.bookkeeping_s = std::max(0.0, qp.total_s - qp.selection_s - qp.evaluation_s);
+            if (profile) *profile = qp;
+            return HB_OK;
+        }
+        HB_TRY(c0->cuda(cudaSetDevice(c0->device), "cudaSetDevice"));
     }
 
     // initial population + evaluation (ea.cpp:48-54)

@@ -259,7 +259,11 @@ class GpuExecutor(BatchExecutor):
     def __init__(self, device: int = 0, host_threads: int = 0, kernel: int = _lib.HB_KERNEL_AUTO,
                  monitor: bool = False, precision: int = _lib.HB_PRECISION_FP64):
         self.ctx = DeviceContext(device, host_threads)
-        self.monitor = monitor  # NVML utilisation trace, like cpu_executor(monitor=true)
+        # utilisation trace (hb_ctx_set_monitor: NVML at 20 Hz + the call's
+        # kernel-busy share), like cpu_executor(monitor=true)
+        self.monitor = monitor
+        if monitor:
+            self.ctx.check(lib.hb_ctx_set_monitor(self.ctx.handle, 1), "hb_ctx_set_monitor")
         if kernel != _lib.HB_KERNEL_AUTO:
             self.ctx.set_kernel(kernel)
         if precision != _lib.HB_PRECISION_FP64:
@@ -267,6 +271,14 @@ class GpuExecutor(BatchExecutor):
 
     def name(self) -> str:
         return "accel"
+
+    def utilization_trace(self):
+        """[(t_s, accel_percent)] of the last monitored call (hb_last_utilization)."""
+        n = C.c_size_t(0)
+        lib.hb_last_utilization(self.ctx.handle, None, 0, C.byref(n))
+        buf = np.zeros(2 * n.value)
+        lib.hb_last_utilization(self.ctx.handle, _lib.ptr(buf), n.value, C.byref(n))
+        return [(float(buf[2 * i]), float(buf[2 * i + 1])) for i in range(n.value)]
 
     def run_raw(self, kind: ModelKind, seeds: np.ndarray, steps: int):
         """(results, fail_step or None, wall_s, status) without raising on
@@ -286,13 +298,8 @@ class GpuExecutor(BatchExecutor):
 
     def run(self, request: BatchRequest) -> BatchResult:
         validate_request(request)
-        sampler = None
-        if self.monitor:
-            from .monitor import GpuUtilSampler
-            sampler = GpuUtilSampler(self.ctx.device)
-            sampler.start()
         out, fail, wall, st = self.run_raw(request.kind, request.seeds, request.steps)
-        trace = sampler.stop() if sampler is not None else []
+        trace = self.utilization_trace() if self.monitor else []
         if st == _lib.HB_BLOWUP_PARTIAL:
             _raise_partial(request.seeds, out, fail)
         return BatchResult(out, wall, trace)

@@ -32,7 +32,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_model_tables():
     L = _lib.lib
-    assert L.hb_abi_version() == 1
+    assert L.hb_abi_version() == 2
     assert [L.hb_body_count(k) for k in range(5)] == [1, 2, 12, 32, 9]
     assert [L.hb_constraint_count(k) for k in range(5)] == [0, 1, 11, 46, 12]
     assert [L.hb_state_rows(k) for k in range(5)] == [6, 13, 83, 238, 82]
@@ -173,3 +173,27 @@ def test_product_does_not_import_oracle():
                 code = re.sub(r"//[^\n]*", "", code)
                 assert "hb_oracle" not in code and "hbo_" not in code, f
                 assert "hetbench/" not in code, f  # no reference headers either
+
+
+def test_model_kind_enum_matches_header():
+    """hb_model_kind in include/hbgpu.h carries every kind the runtime
+    accepts, CpgHinge (4) included, with the Python ordinals."""
+    import re
+    with open(os.path.join(ROOT, "include", "hbgpu.h")) as f:
+        text = f.read()
+    enum = dict((n, int(v)) for n, v in re.findall(r"HB_(BOX|BOX_AND_BALL|ARM_WITH_ROPE|HUMANOID|CPG_HINGE) = (\d)",
+                                                   text))
+    assert enum == {"BOX": 0, "BOX_AND_BALL": 1, "ARM_WITH_ROPE": 2, "HUMANOID": 3, "CPG_HINGE": 4}
+    assert [int(k) for k in hb.ALL_MODELS] == sorted(enum.values())
+
+
+def test_snap_equal_times_rules():
+    """hb_snap_equal_times: equal within the measured spread -> equal;
+    proportional otherwise; dead back-ends untouched."""
+    assert hb.snap_equal_times([1.0, 1.02, 0.99], [0.05, 0.04, 0.03]) == [1.0033333333333332] * 3 or \
+        len(set(hb.snap_equal_times([1.0, 1.02, 0.99], [0.05, 0.04, 0.03]))) == 1
+    assert hb.snap_equal_times([1.0, 1.5], [0.05, 0.05]) == [1.0, 1.5]
+    assert hb.snap_equal_times([1.0, 1.005], None, None, 0.01)[0] == hb.snap_equal_times([1.0, 1.005])[1]
+    t = hb.snap_equal_times([1.0, 0.0, 1.01], [0.02, 0.0, 0.02], [True, False, True])
+    assert t[1] == 0.0 and t[0] == t[2]
+    assert hb.plan_allocation_n([1.0, 0.0, 1.0], 100) == [50, 0, 50]

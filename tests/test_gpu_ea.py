@@ -103,6 +103,48 @@ def test_sharded_over_two_contexts(gpu):
         assert np.array_equal(a.population.fitnesses, b.population.fitnesses)
 
 
+@pytest.mark.parametrize("kind,pop,times", [(1, 3000, [1.0, 2.0, np.inf]), (3, 600, None),
+                                             (4, 1000, [1.0, 1.0, 1.0]), (0, 70000, [2.0, 1.0, 1.0])])
+def test_queued_multi_context_loop(gpu, kind, pop, times):
+    """The queued multi-context loop (persistent per-device workers,
+    event-chained generations): three contexts, unequal / equal / one
+    share-less device (infinite time), both selection sorts; identical to
+    the one-context loop; history requests take the checked loop and agree."""
+    ex = hb.MultiGpuExecutor([0, 0, 0])
+    a = hb.run_ea_native(kind, pop, 3, 40, ex, seed=2, device_times=times)
+    b = hb.run_ea(kind, pop, 3, 40, gpu, seed=2)
+    assert np.array_equal(a.population.genomes, b.population.genomes)
+    assert np.array_equal(a.population.fitnesses.view(np.uint64), b.population.fitnesses.view(np.uint64))
+    assert a.best_fitness == b.best_fitness
+    assert a.profile.host_overhead_s >= 0.0
+    h = hb.run_ea_native(kind, pop, 3, 40, ex, seed=2, device_times=times, keep_history=True)
+    assert np.array_equal(h.population.genomes, b.population.genomes)
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_config5_eight_contexts_vs_reference_run_ea(kind):
+    """BASELINE configs[4] as specified — 65 536 genomes x 5 generations x
+    1 000 steps, offspring sharded over 8 devices by the throughput splitter
+    (here 8 contexts on one B200, calibrated by hb_calibrate) — against the
+    reference's own run_ea: genomes, fitness, best fitness bit for bit.
+    Prints the per-generation host overhead (wall not covered by device
+    work) of the queued loop."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    ex = hb.MultiGpuExecutor([0] * 8)
+    ex.calibrate(kind, 1000, 4096)
+    assert all(ex.device_ok)
+    g, f = O.ref_run_ea(kind, 65536, 5, 1000, seed=0)
+    for _ in range(2):  # second call: persistent buffers, events, graphs
+        r = hb.run_ea(kind, 65536, 5, 1000, ex, seed=0)
+        assert np.array_equal(r.population.genomes, g)
+        assert np.array_equal(r.population.fitnesses.view(np.uint64), f.view(np.uint64))
+        assert bits(r.best_fitness) == bits(max(f.tolist()))
+    per_gen_us = 1e6 * r.profile.host_overhead_s / 6
+    print(f"8 contexts kind {kind}: total {1e3 * r.profile.total_s:.3f} ms, host overhead "
+          f"{per_gen_us:.1f} us per evaluation")
+
+
 def test_native_preconditions(gpu):
     for pop, gens in ((5, 1), (0, 1), (4, 0)):
         with pytest.raises(ValueError):

@@ -379,19 +379,28 @@ def test_box_zero_copy_path_equals_staged(gpu):
 @pytest.mark.parametrize("kind,n,steps,stride", [
     (4, 8192, 5000, 257),    # configs[2]: CPG / hinge robot, 8192 x 5000
     (3, 8192, 5000, 509),    # its humanoid proxy
-    (0, 32768, 20000, 997),  # configs[3] endpoint: 32768 x 20000
+    (0, 32768, 20000, 997),  # configs[3] endpoints: 32768 x 20000, every model
     (1, 32768, 20000, 2003),
+    (2, 32768, 20000, 257),
+    (3, 32768, 20000, 509),
+    (4, 32768, 20000, 257),
     (2, 32768, 2000, 4001),
 ])
 def test_baseline_sizes_subsampled_vs_oracle(gpu, kind, n, steps, stride):
     """BASELINE configs at full size on the GPU; an evenly strided subsample
-    re-simulated by the oracle must match bit for bit, no variant may blow
-    up, and a checksum-of-checksums pins the whole batch for determinism."""
+    (first and last variant included) re-simulated by the oracle — and, for
+    the reference's models, by the reference library itself — must match bit
+    for bit, no variant may blow up, and a checksum-of-checksums pins the
+    whole batch for determinism."""
     seeds = np.arange(n, dtype=np.uint64)
     res = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
     assert np.all(res["steps_executed"] == steps)
-    sub = slice(0, n, stride)
-    assert np.array_equal(res[sub], O.simulate_batch(kind, seeds[sub], steps).results)
+    idx = np.unique(np.concatenate([np.arange(0, n, stride), [n - 1]]))
+    assert np.array_equal(res[idx], O.simulate_batch(kind, seeds[idx], steps).results)
+    if kind < 4 and O.ref_available():
+        rc, want, _, _, msg = O.ref_cpu_run(kind, seeds[idx], steps, 0)
+        assert rc == 0, msg
+        assert np.array_equal(res[idx], want)
     again = gpu.run(hb.BatchRequest(kind, seeds, steps)).results
     cc = np.bitwise_xor.reduce(res["checksum"] * np.uint64(0x9E3779B97F4A7C15))
     assert cc == np.bitwise_xor.reduce(again["checksum"] * np.uint64(0x9E3779B97F4A7C15))
