@@ -64,6 +64,9 @@ class PhaseProfile:
     evaluation_s: float = 0.0
     bookkeeping_s: float = 0.0
     total_s: float = 0.0
+    # native loop only: wall time not covered by device work (host launch,
+    # sync and bookkeeping cost); not part of ea.cpp's profile
+    host_overhead_s: float = 0.0
 
     def evaluation_fraction(self) -> float:
         return self.evaluation_s / self.total_s if self.total_s > 0.0 else 0.0
@@ -187,7 +190,7 @@ def run_ea_native(kind: ModelKind, population_size: int, generations: int, steps
     if st != _lib.HB_OK:
         raise RuntimeError(f"hb_run_ea failed [{st}]: {ctxs[0].error()}")
     profile = PhaseProfile(prof.selection_s, prof.variation_s, prof.evaluation_s,
-                           prof.bookkeeping_s, prof.total_s)
+                           prof.bookkeeping_s, prof.total_s, prof.host_overhead_s)
     history = [] if hg is None else [(hg[g], hf[g]) for g in range(generations + 1)]
     return EaResult(Population(gen, fit, generations), profile, float(best.value), history)
 

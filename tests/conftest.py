@@ -26,3 +26,12 @@ def gpu():
     ex = GpuExecutor(0)
     yield ex
     ex.ctx.close()
+
+
+@pytest.fixture(scope="session")
+def gpu_generic():
+    """The reference-order generic kernel variant (the in-tree cross-check)."""
+    from paper_2502_11129_b200 import GpuExecutor
+    ex = GpuExecutor(0, kernel=1)
+    yield ex
+    ex.ctx.close()

@@ -6,8 +6,10 @@ bit-exact by design.  Stated tolerance against the FP64 reference
     max over 32 768 variants: 2.5e-5);
   * humanoid, cpg_hinge (stiffer coupled dynamics amplify FP32 correction
     noise in a few contact-heavy variants): >= 99 % of variants within
-    1e-4, median within 1e-5, every variant within 0.05 m absolute
-    (measured over 32 768: 0.14 % / 0.06 % above 1e-4, worst 1.3 cm);
+    1e-4, median within 1e-5, and EVERY variant within a per-model relative
+    bound — humanoid 5e-3, cpg_hinge 2e-2 (measured over 32 768 x 1 000,
+    profiles/r01_fp32_mode_v9.json: max 2.2e-3 / 1.3e-2; 0.14 % / 0.06 %
+    of variants above 1e-4);
   * the same variants complete, and the (mu + lambda) parent set of a
     65 536-genome population keeps >= 99 % of the reference's (measured:
     100 %; the parent RANKS differ in 2-4 %, so later generations diverge —
@@ -23,6 +25,7 @@ from paper_2502_11129_b200 import _lib
 pytestmark = pytest.mark.gpu
 
 RTOL = 1e-4
+RTOL_MAX = {3: 5e-3, 4: 2e-2}  # per-variant bound for the coupled models
 
 
 @pytest.fixture(scope="module")
@@ -52,7 +55,7 @@ def test_fp32_fitness_within_tolerance(fp32, kind, n, steps):
         assert err.max() <= RTOL, (kind, steps, float(err.max()))
     else:
         assert np.mean(err <= RTOL) >= 0.99 and np.median(err) <= 1e-5, (kind, steps)
-        assert np.abs(got["fitness"] - want.results["fitness"]).max() <= 0.05
+        assert err.max() <= RTOL_MAX[kind], (kind, steps, float(err.max()))
 
 
 def test_fp32_known_answers(fp32):

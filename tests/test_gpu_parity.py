@@ -218,6 +218,7 @@ def test_multi_device_degraded_redispatch(kind):
         ex.run(hb.BatchRequest(kind, seeds, 120))
     for c in ex.ctxs:
         c.inject_fault(hb._lib.HB_FAULT_NONE)
+    ex.shares = None  # even split: index 4321 lies in context 1's slice [2500, 5000)
     ex.ctxs[1].inject_fault(hb._lib.HB_FAULT_BLOWUP, int(seeds[4321]))
     with pytest.raises(hb.BatchFailure) as e:
         ex.run(hb.BatchRequest(kind, seeds, 120))
@@ -247,13 +248,6 @@ def test_calibrate_contexts_events_and_snap():
 def test_fp64_probe(gpu):
     ops, ms = gpu.ctx.fp64_peak()
     assert ms > 0 and 1e12 < ops < 1e14
-
-
-@pytest.fixture(scope="module")
-def gpu_generic():
-    ex = hb.GpuExecutor(0, kernel=1)
-    yield ex
-    ex.ctx.close()
 
 
 @pytest.mark.parametrize("kind,n,steps", [(0, 200000, 300), (1, 65536, 200), (2, 16384, 100),

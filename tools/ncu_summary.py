@@ -22,6 +22,11 @@ def summary(path):
     for k in KEYS:
         if k in d:
             res[k] = d[k][0] + " " + d[k][1]
+    # every FP64 / XU (MUFU) pipe counter the capture holds: the ratio of
+    # pipe cycles to instructions says what one FP64 instruction costs
+    for k, (x, uu) in d.items():
+        if ("fp64" in k or "pipe_xu" in k) and (k.endswith(".sum") or "pct_of_peak" in k) and k not in res:
+            res[k] = x + " " + uu
     stalls = {}
     for k, (x, _) in d.items():
         if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
