@@ -9,7 +9,7 @@
     for all four models, kernel-only and e2e rates;
   * reference CPU rate per model on the host cores (bounded sample).
 
-    python tools/sweep.py --out profiles/r01_sweeps.json [--quick]
+    python tools/sweep.py --out profiles/r02_sweeps.json [--quick]
 """
 import argparse
 import json
