@@ -163,6 +163,15 @@ hb_status hb_last_utilization(const hb_ctx* ctx, hb_util_sample* out, size_t cap
 #define HB_FAULT_DEVICE 2
 hb_status hb_ctx_inject_fault(hb_ctx* ctx, int mode, uint64_t seed);
 
+/* Start-up reservation: size every device and pinned staging buffer for
+ * batches of up to `n` variants of `kind` and load the kernel such a batch
+ * runs (one discarded 1-step batch of seeds 0..n-1).  A context's first call
+ * at a new size otherwise pays its allocations and the lazy kernel load in
+ * its wall_time_s (tools/cold_probe.py: 17-85 ms against 0.5-12 ms warm at
+ * the sweep sizes), which a single-probe calibrate (scheduler.cpp:30-56)
+ * reads as accelerator speed.  Optional; hb_run_batch grows on demand. */
+hb_status hb_ctx_reserve(hb_ctx* ctx, int kind, size_t n);
+
 /* Page-locked host memory (cudaHostAlloc, portable + mapped).  hb_run_batch / hb_fetch
  * DMA the results straight into an `out` buffer allocated here (no staging
  * copy); any other buffer goes through the context's staging buffer. */

@@ -92,6 +92,14 @@ public:
     std::string name() const override { return "accel"; }
     hb_ctx* context() { return ctx_; }
 
+    // Start-up reservation (hb_ctx_reserve): buffers sized and the kernel
+    // loaded for batches of up to n variants of `kind`, so the first timed
+    // run() — e.g. calibrate's single probe (scheduler.cpp:30-56) — is warm.
+    void reserve(hetbench::ModelKind kind, std::size_t n) {
+        if (hb_ctx_reserve(ctx_, static_cast<int>(kind), n) != HB_OK)
+            throw std::runtime_error(std::string("gpu_executor: ") + hb_last_error(ctx_));
+    }
+
 private:
     hb_ctx* ctx_ = nullptr;
     bool monitor_ = true;

@@ -32,7 +32,7 @@ EXPORTED = (
     "hb_last_launch_stats", "hb_run_ea", "hb_eval_device", "hb_ea_init_genomes",
     "hb_ea_select_vary", "hb_host_alloc", "hb_host_free", "hb_last_fail_steps",
     "hb_ctx_set_zero_copy", "hb_ctx_set_precision", "hb_work_counter", "hb_ctx_inject_fault",
-    "hb_calibrate", "hb_snap_equal_times", "hb_ctx_set_monitor", "hb_last_utilization",
+    "hb_calibrate", "hb_snap_equal_times", "hb_ctx_set_monitor", "hb_last_utilization", "hb_ctx_reserve",
 )
 
 HB_KERNEL_AUTO, HB_KERNEL_GENERIC = 0, 1
@@ -86,6 +86,7 @@ def _load():
         "hb_run_batch_multi": (i32, [vp, i32, vp, i32, vp, sz, u64, vp, vp, vp, P(dbl), vp, vp]),
         "hb_calibrate": (i32, [vp, i32, i32, u64, u64, i32, vp, vp, vp]),
         "hb_ctx_set_monitor": (i32, [vp, i32]),
+        "hb_ctx_reserve": (i32, [vp, i32, sz]),
         "hb_last_utilization": (i32, [vp, vp, sz, P(sz)]),
         "hb_snap_equal_times": (i32, [vp, vp, vp, i32, dbl, vp]),
         "hb_fp64_peak": (i32, [vp, P(dbl), P(dbl)]),

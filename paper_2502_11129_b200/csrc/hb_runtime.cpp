@@ -1108,6 +1108,17 @@ static hb_status run_batch_impl(hb_ctx* c, int kind, const uint64_t* seeds, size
     return HB_OK;
 }
 
+hb_status hb_ctx_reserve(hb_ctx* c, int kind, size_t n) {
+    if (!c) return set_global(HB_INVALID_ARG, "null context");
+    if (n == 0) return HB_OK;
+    std::vector<uint64_t> seeds(n);
+    for (size_t i = 0; i < n; ++i) seeds[i] = i;
+    std::vector<hb_variant_result> out(n);
+    const hb_status st =
+        run_batch_impl(c, kind, seeds.data(), n, 1, out.data(), nullptr, nullptr, std::chrono::steady_clock::now());
+    return st == HB_BLOWUP_PARTIAL ? HB_OK : st;
+}
+
 hb_status hb_ctx_set_monitor(hb_ctx* c, int enable) {
     if (!c) return set_global(HB_INVALID_ARG, "null context");
     if (!enable) {

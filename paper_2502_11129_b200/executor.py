@@ -272,6 +272,12 @@ class GpuExecutor(BatchExecutor):
     def name(self) -> str:
         return "accel"
 
+    def reserve(self, kind: ModelKind, n: int) -> None:
+        """Size the context's buffers for batches of up to n variants of kind
+        and load their kernel (hb_ctx_reserve): start-up work a single-probe
+        calibrate would otherwise time as accelerator speed."""
+        self.ctx.check(lib.hb_ctx_reserve(self.ctx.handle, int(kind), int(n)), "hb_ctx_reserve")
+
     def utilization_trace(self):
         """[(t_s, accel_percent)] of the last monitored call (hb_last_utilization)."""
         n = C.c_size_t(0)

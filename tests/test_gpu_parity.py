@@ -334,6 +334,27 @@ def test_humanoid_blowup_final_state(gpu, gpu_generic):
     assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3])
 
 
+def test_reserve_then_run_is_identical():
+    """hb_ctx_reserve (start-up sizing + kernel load through one discarded
+    1-step batch) leaves no trace in later results: a reserved context's
+    batches equal a fresh context's, below, at and above the reserved size."""
+    a = hb.GpuExecutor(0)
+    b = hb.GpuExecutor(0)
+    try:
+        for kind, n in ((0, 70000), (1, 4096), (3, 1000), (4, 3000)):
+            a.reserve(kind, n)
+            for m in (n // 3, n, n + 17):
+                seeds = np.arange(m, dtype=np.uint64) + np.uint64(99)
+                ra = a.run(hb.BatchRequest(kind, seeds, 50)).results
+                rb = b.run(hb.BatchRequest(kind, seeds, 50)).results
+                assert np.array_equal(ra, rb)
+        with pytest.raises(Exception):
+            a.reserve(9, 10)
+    finally:
+        a.ctx.close()
+        b.ctx.close()
+
+
 def test_box_nan_state_fails_at_step_one(gpu):
     """A NaN x / y / velocity coordinate (which p.z >= 0 does not catch) keeps
     the warp out of the proven Box phases: the blow-up is reported at step 1,

@@ -17,6 +17,7 @@
 // Built by `make -C oracle sweep` from the reference sources in place into
 // oracle/_ref/ref_sweep (git-ignored; travels to the GPU box prebuilt).
 //   usage: ref_sweep <config.toml> <output_dir> [device]
+#include <algorithm>
 #include <cstdio>
 #include <fstream>
 #include <map>
@@ -42,8 +43,19 @@ int main(int argc, char** argv) {
         cfg.output_dir = argv[2];
         validate_config(cfg);
         SweepHooks hooks;
-        hooks.make_accel = [device](const SweepConfig&) -> std::unique_ptr<batch_executor> {
-            return std::make_unique<hbgpu::gpu_executor>(device, /*monitor=*/true);
+        // start-up: every model's buffers sized for its largest variant count
+        // and its kernels loaded (hb_ctx_reserve), so the sweep's first rows
+        // and calibrate's single probe time warm calls, as a long-running
+        // accelerator service would serve them
+        hooks.make_accel = [device](const SweepConfig& c) -> std::unique_ptr<batch_executor> {
+            auto ex = std::make_unique<hbgpu::gpu_executor>(device, /*monitor=*/true);
+            for (const auto& [model, counts] : c.variants_per_model) {
+                std::uint64_t mx = 0;
+                for (std::uint64_t v : counts) mx = std::max(mx, v);
+                if (c.hybrid_probe_n > mx) mx = c.hybrid_probe_n;
+                ex->reserve(model, mx);
+            }
+            return ex;
         };
         const std::uint64_t total = expected_row_count(cfg);
         std::uint64_t seen = 0;
