@@ -62,6 +62,10 @@ def parse():
                          "loop per step (configs[4]: evaluate, fitness gather, select)")
     ap.add_argument("--population", type=int, default=65536, help="ea: population size (global)")
     ap.add_argument("--generations", type=int, default=5, help="ea: generations per step")
+    ap.add_argument("--precision", default="fp64", choices=["fp64", "fp32"],
+                    help="fp64 = the bit-exact product path; fp32 = the opt-in FP32 throughput mode "
+                         "(multi-body models; SURVEY §8 f3): the line adds its fitness error and EA "
+                         "selection agreement against the FP64 product on the same seeds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -69,7 +73,8 @@ def parse():
 
 def workload_name(a):
     tag = " (BASELINE configs[1])" if (a.model, a.variants, a.sim_steps) == ("box", 16384, 1000) else ""
-    return f"{a.model} {a.variants} variants x {a.sim_steps} steps per GPU{tag}"
+    mode = " [FP32 mode]" if getattr(a, "precision", "fp64") == "fp32" and a.model != "box" else ""
+    return f"{a.model} {a.variants} variants x {a.sim_steps} steps per GPU{tag}{mode}"
 
 
 # --------------------------------------------------------------------- clocks
@@ -347,7 +352,9 @@ def run_ours(a, ws, rank, local):
     # (calibrate_ranks), the times are all-gathered, and plan_allocation_n
     # gives each rank a contiguous share in proportion to its throughput.
     n_total = a.variants * ws
-    ex = hb.GpuExecutor(local)
+    from paper_2502_11129_b200 import _lib as _hl
+    fp32 = a.precision == "fp32"
+    ex = hb.GpuExecutor(local, precision=_hl.HB_PRECISION_FP32 if fp32 else _hl.HB_PRECISION_FP64)
     calib = None
     if ws > 1:
         from paper_2502_11129_b200 import distributed as hbd
@@ -414,6 +421,10 @@ def run_ours(a, ws, rank, local):
 
     # ---- roofline: FP64 pipe (measured probe on this device) ----
     peak_ops, _ = ctx.fp64_peak()
+    if fp32 and a.model != "box":
+        # FP32 mode: float-float positions on the FP32 pipe; nominal peak =
+        # 148 SMs x 128 FP32 lanes x the SM clock sampled during the run
+        peak_ops = 148 * 128 * 1e6 * (clk.get("sm_mhz") or 1965.0)
     per_gpu_rate = n * a.sim_steps / (float(np.mean(kernel_ms)) * 1e-3)
     achieved = W_ALG[a.model] * per_gpu_rate
     traffic = load_traffic(a.model, a.variants, a.sim_steps)
@@ -426,13 +437,16 @@ def run_ours(a, ws, rank, local):
     # W_alg is their (conservative) count.
     exec_rate = None if ops_exec is None else ops_exec / kmean_s
     head = exec_rate if exec_rate is not None else achieved
-    roof = {"bound": "fp64", "achieved": head / 1e12, "peak": peak_ops / 1e12,
+    roof = {"bound": "fp32" if fp32 and a.model != "box" else "fp64",
+            "achieved": head / 1e12, "peak": peak_ops / 1e12,
             "unit": "TFLOP/s", "frac": head / peak_ops, "traffic": traffic,
             "ops_basis": "executed (hb_work_counter)" if exec_rate is not None else "W_alg (SURVEY.md §8d)",
             "achieved_w_alg": achieved / 1e12, "frac_w_alg": achieved / peak_ops,
             "algorithmic_ops_per_variant_step": W_ALG[a.model],
-            "peak_source": "measured on this device by hb_fp64_peak (DMUL+DADD stream, no FMA); "
-                           "MEASURED_PEAKS.json has no FP64 figure",
+            "peak_source": ("nominal 148 SM x 128 FP32 lanes x sampled SM clock (FP32 mode)"
+                            if fp32 and a.model != "box" else
+                            "measured on this device by hb_fp64_peak (DMUL+DADD stream, no FMA); "
+                            "MEASURED_PEAKS.json has no FP64 figure"),
             "kernel": hb.kernel_name(kind, n),
             "kernel_ms_mean": float(np.mean(kernel_ms)),
             "exact_step_replays": replays,
@@ -505,6 +519,24 @@ def run_ours(a, ws, rank, local):
                                                           " (host init + H2D + kernel + D2H)"),
                "python_mirror_ms_per_step": 1e3 * t_py / a.steps}
 
+    # ---- FP32 mode: tolerance and selection agreement vs the FP64 product ----
+    fp32_check = None
+    if fp32 and rank == 0:
+        ex64 = hb.GpuExecutor(local)
+        f64 = ex64.run(hb.BatchRequest(kind, seeds, a.sim_steps)).results["fitness"]
+        f32 = out["fitness"]
+        rel = np.abs(f32 - f64) / np.maximum(np.abs(f64), 1e-3)
+        mu = n // 2  # (mu + lambda) parents of this batch as a population (ea.cpp:60-72)
+        o32 = np.argsort(-f32, kind="stable")[:mu]
+        o64 = np.argsort(-f64, kind="stable")[:mu]
+        fp32_check = {"vs": "FP64 product (bit-exact with the reference) on the same seeds",
+                      "max_rel_fitness_err": float(rel.max()), "median_rel_fitness_err": float(np.median(rel)),
+                      "frac_rel_err_above_1e-4": float(np.mean(rel > 1e-4)),
+                      "parent_set_overlap": len(set(o32.tolist()) & set(o64.tolist())) / max(1, mu),
+                      "parent_rank_identical_fraction": float(np.mean(o32 == o64)),
+                      "stated_tolerance": "tests/test_gpu_fp32.py (DESIGN.md §4.1)"}
+        ex64.ctx.close()
+
     cpu = None
     if rank == 0 and ws == 1 and not a.no_cpu_baseline:
         try:
@@ -515,7 +547,8 @@ def run_ours(a, ws, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "variant-steps/s", "n_gpus": ws,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 (float-float positions)" if fp32 and a.model != "box" else "f64",
                 "data": "synthetic (seeds 0..N-1 through build_model; no datasets)",
                 "config": {"workload": workload_name(a), "model": a.model,
                            "variants_per_gpu": a.variants, "global_variants": n_total,
@@ -528,7 +561,11 @@ def run_ours(a, ws, rank, local):
                                  "event pair)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
                 "gpu_launches": a.steps, "e2e_gpu_launches": a.steps if e2e else 0,
-                "bracket_wall_s": wall_region, "parity": "bit-exact FP64 vs reference"}
+                "bracket_wall_s": wall_region,
+                "parity": ("FP32 mode: within the stated tolerance, see fp32" if fp32 and a.model != "box"
+                           else "bit-exact FP64 vs reference")}
+        if fp32_check is not None:
+            line["fp32"] = fp32_check
         print(json.dumps(line))
     ex.ctx.close()
     if dist is not None:
