@@ -589,7 +589,10 @@ def run_ea_bench(a, ws, rank, local, dist, dev, red_dev, kind):
     pop, G = a.population, a.generations
     evaluated = pop + G * (pop // 2)
     if ws > 1:
-        ex = hb.MultiGpuExecutor(list(range(ws))) if rank == 0 else None
+        # one context per GPU (modulo the visible devices: several ranks per
+        # GPU only in the gloo tests)
+        ngpu = max(1, torch.cuda.device_count())
+        ex = hb.MultiGpuExecutor([d % ngpu for d in range(ws)]) if rank == 0 else None
         calib = ex.calibrate(kind, a.sim_steps, max(1, (pop // 2) // ws)) if rank == 0 else None
     else:
         ex = hb.GpuExecutor(local)

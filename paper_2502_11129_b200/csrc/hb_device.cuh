@@ -13,22 +13,9 @@
 namespace hb {
 namespace {
 
-struct Coefs {
-    double dt, gdt, damp, inv_dt, half_k_stiff, half_k_soft;
-};
+using Coefs = StepCoefs;
 
-__device__ __forceinline__ Coefs make_coefs(double dt) {
-    Coefs c;
-    c.dt = dt;
-    c.gdt = kGravity * dt;          // v.z -= kGravity * dt        (simkernel.cpp:130)
-    c.damp = 1.0 - kDamping * dt;   // damp = 1 - damping * dt     (:126)
-    c.inv_dt = 1.0 / dt;            // (:156)
-    const double ks = (kStiffLink * dt) * dt;  // c.stiffness * dt * dt (:145)
-    const double kf = (kSoftLink * dt) * dt;
-    c.half_k_stiff = 0.5 * (ks < 1.0 ? ks : 1.0);  // std::min(1.0, x), then 0.5 * k (:146)
-    c.half_k_soft = 0.5 * (kf < 1.0 ? kf : 1.0);
-    return c;
-}
+__device__ __forceinline__ Coefs make_coefs(double dt) { return step_coefs(dt); }
 
 __device__ __forceinline__ uint64_t absorb(uint64_t h, double x) {
     return fnv_absorb_bits(h, static_cast<uint64_t>(__double_as_longlong(x)));

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include "../../include/hbgpu.h"
+#include "hb_model.h"
 
 namespace hb {
 
@@ -18,6 +19,27 @@ namespace hb {
 //  fail:  n x first failing step (0 = completed).
 //  counters: [0] += #failed variants, [1] += #exact step replays.
 //  final_state (nullable): SoA rows, ld.
+// Loop-invariant step coefficients (hoisting them is value-preserving;
+// SURVEY.md §8 a3): computed on the host per launch and passed in the kernel
+// parameters, so the stepping kernels read them as constant-bank operands
+// instead of holding six doubles in registers for the whole horizon.
+struct StepCoefs {
+    double dt, gdt, damp, inv_dt, half_k_stiff, half_k_soft;
+};
+
+HB_HD StepCoefs step_coefs(double dt) {
+    StepCoefs c{};
+    c.dt = dt;
+    c.gdt = kGravity * dt;          // v.z -= kGravity * dt        (simkernel.cpp:130)
+    c.damp = 1.0 - kDamping * dt;   // damp = 1 - damping * dt     (:126)
+    c.inv_dt = 1.0 / dt;            // (:156)
+    const double ks = (kStiffLink * dt) * dt;  // c.stiffness * dt * dt (:145)
+    const double kf = (kSoftLink * dt) * dt;
+    c.half_k_stiff = 0.5 * (ks < 1.0 ? ks : 1.0);  // std::min(1.0, x), then 0.5 * k (:146)
+    c.half_k_soft = 0.5 * (kf < 1.0 ? kf : 1.0);
+    return c;
+}
+
 struct SimArgs {
     const double* init;
     const uint64_t* seeds;
@@ -40,6 +62,8 @@ struct SimArgs {
     // instead of the VariantResult records — the generation loop's
     // evaluation, which needs nothing else
     double* fitness = nullptr;
+    // step_coefs(dt), filled by launch_sim for the multi-body kernels
+    StepCoefs k{};
 };
 
 cudaError_t launch_sim(int kind, const SimArgs& a, cudaStream_t st, int sms, int variant);

@@ -19,6 +19,10 @@ def main():
     for kind in range(5):
         seeds = rng.integers(0, 2**63, 1000, dtype=np.uint64)
         ex.run(hb.BatchRequest(kind, seeds, 20))
+    # the saturated-regime shapes (register-capped multibody kernels, U = 1 / 2)
+    for kind, n in ((1, 65536), (2, 65536), (4, 65536)):
+        ex.run(hb.BatchRequest(kind, np.arange(n, dtype=np.uint64), 2))
+    ex.reserve(3, 4096)
     hb.run_ea(0, 4096, 2, 20, ex, seed=1)
     hb.run_ea(0, 70000, 1, 5, ex, seed=1)
     hb.run_ea(1, 2048, 2, 10, ex, seed=1)
