@@ -1,4 +1,4 @@
-# round-2 final measurement pass (kernels as committed): tests, sanitizer,
+# round measurement pass (run under gpurun from the repo root): GPU tests, sanitizer,
 # the round profile, saturated rates, FP32-mode lines, ncu captures
 # (summarised on the box; .ncu-rep files are too large to ship back)
 mkdir -p gpurun_out/ncu
