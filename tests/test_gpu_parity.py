@@ -182,6 +182,36 @@ def test_full_size_properties(gpu):
     assert np.array_equal(out, r1)
 
 
+@pytest.mark.parametrize("kind,n", [(0, 16384), (1, 32768), (2, 32768), (3, 8192), (4, 8192)])
+def test_full_size_state_properties(gpu, kind, n):
+    """Size-independent properties at BASELINE batch sizes, on the final
+    states (hb_run_states from build_model states): no body below the ground
+    (the end-of-sweep clamp, simkernel.cpp:150-151; test_simkernel.cpp:154-162),
+    every coordinate finite and inside the blow-up limit, and — for the
+    reference models — composition: S + T steps in one launch equal T steps
+    resumed from the state after S (bit for bit, final states and checksums),
+    i.e. nothing outside the state rows carries over between steps."""
+    seeds = np.arange(n, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+    soa = hb.build_states(kind, seeds)
+    nb, m = hb.body_count(kind), hb.constraint_count(kind)
+    pos = soa[: 3 * nb].T.reshape(n, nb, 3)
+    vel = soa[3 * nb: 6 * nb].T.reshape(n, nb, 3)
+    rest = soa[6 * nb: 6 * nb + m].T
+    cpg = soa[6 * nb + m:].T if kind == 4 else None
+    S, T = 600, 400
+    r_all, f_all, p_all, v_all = gpu.run_states(kind, pos, vel, rest, steps=S + T, seeds=seeds, cpg=cpg)
+    assert np.all(f_all == 0)
+    assert np.all(p_all[:, :, 2] >= 0.0)
+    assert np.all(np.isfinite(p_all)) and np.all(np.abs(p_all) <= 1e6) and np.all(np.abs(v_all) <= 1e6)
+    if kind == 4:
+        return  # the CPG state is not among the returned rows
+    _, f1, p1, v1 = gpu.run_states(kind, pos, vel, rest, steps=S, seeds=seeds)
+    r2, f2, p2, v2 = gpu.run_states(kind, p1, v1, rest, steps=T, seeds=seeds)
+    assert np.all(f1 == 0) and np.all(f2 == 0)
+    assert np.array_equal(p2, p_all) and np.array_equal(v2, v_all)
+    assert np.array_equal(r2["checksum"], r_all["checksum"])
+
+
 def test_multi_device_executor_single_gpu():
     ex = hb.MultiGpuExecutor([0])
     seeds = np.arange(3000, dtype=np.uint64)
