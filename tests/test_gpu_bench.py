@@ -49,3 +49,29 @@ def test_bench_ea_line():
                "--steps", "3", "--warmup", "3")
     assert KEYS - {"roofline"} <= set(d)  # the loop line reports phases, not a kernel roofline
     assert d["value"] > 0 and d["host_overhead_us_per_generation"] >= 0
+
+
+def _bench_ranks(nproc, port, *args):
+    env = dict(os.environ, HB_DIST_BACKEND="gloo")  # several ranks on one GPU: gloo, not NCCL
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", str(nproc), *args]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_two_ranks_batch_and_ea():
+    """The multi-rank paths the driver's scaling run takes (torchrun, one
+    rank per GPU; here two ranks share GPU 0 over gloo): calibrated shares,
+    the max-over-ranks line, and the in-process N-context generation loop."""
+    d = _bench_ranks(2, 29531, "--variants", "4096", "--sim-steps", "100", "--steps", "3", "--warmup", "3",
+                     "--no-cpu-baseline")
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    shares = d["config"]["splitter"]["shares"]
+    assert sum(shares) == 8192 and len(shares) == 2
+    e = _bench_ranks(2, 29532, "--workload", "ea", "--population", "4096", "--generations", "2",
+                     "--sim-steps", "100", "--steps", "3", "--warmup", "3")
+    assert e["n_gpus"] == 2 and e["value"] > 0
+    assert all(e["config"]["splitter"]["device_ok"])
