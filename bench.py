@@ -55,7 +55,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="box", choices=MODELS)
-    ap.add_argument("--variants", type=int, default=16384, help="variants per GPU")
+    ap.add_argument("--variants", type=int, default=16384,
+                    help="variants per GPU (weak scaling) or in total (--scaling strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: --variants per GPU (the default line); strong: --variants in total, "
+                         "split over the GPUs by the splitter (BASELINE configs[3]: 32768 variants at "
+                         "1/2/4/8 GPUs)")
     ap.add_argument("--sim-steps", type=int, default=1000)
     ap.add_argument("--workload", default="batch", choices=["batch", "ea"],
                     help="batch = one simulate() pass per step (configs[1]); ea = full generation "
@@ -72,9 +77,15 @@ def parse():
 
 
 def workload_name(a):
-    tag = " (BASELINE configs[1])" if (a.model, a.variants, a.sim_steps) == ("box", 16384, 1000) else ""
+    strong = getattr(a, "scaling", "weak") == "strong"
+    tag = ""
+    if (a.model, a.variants, a.sim_steps) == ("box", 16384, 1000) and not strong:
+        tag = " (BASELINE configs[1])"
+    elif a.variants == 32768 and strong:
+        tag = " (BASELINE configs[3] point)"
     mode = " [FP32 mode]" if getattr(a, "precision", "fp64") == "fp32" and a.model != "box" else ""
-    return f"{a.model} {a.variants} variants x {a.sim_steps} steps per GPU{tag}{mode}"
+    per = "in total, split over the GPUs" if strong else "per GPU"
+    return f"{a.model} {a.variants} variants x {a.sim_steps} steps {per}{tag}{mode}"
 
 
 # --------------------------------------------------------------------- clocks
@@ -273,7 +284,7 @@ def run_reference(a, ws, rank):
                      "vs_baseline": None, "scaling": "strong"})
         print(json.dumps(base))
         return
-    n_total = a.variants * a.gpus
+    n_total = a.variants * a.gpus if a.scaling == "weak" else a.variants
     # bounded per-step sample: ~10 s of host time per step at most
     per_vs_core_ns = PER_VS_CORE_NS[k]
     max_vs = 10.0 * cores / (per_vs_core_ns * 1e-9)
@@ -351,14 +362,14 @@ def run_ours(a, ws, rank, local):
     # retargeted to N GPUs: every rank times the same probe on its own GPU
     # (calibrate_ranks), the times are all-gathered, and plan_allocation_n
     # gives each rank a contiguous share in proportion to its throughput.
-    n_total = a.variants * ws
+    n_total = a.variants * ws if a.scaling == "weak" else a.variants
     from paper_2502_11129_b200 import _lib as _hl
     fp32 = a.precision == "fp32"
     ex = hb.GpuExecutor(local, precision=_hl.HB_PRECISION_FP32 if fp32 else _hl.HB_PRECISION_FP64)
     calib = None
     if ws > 1:
         from paper_2502_11129_b200 import distributed as hbd
-        calib = hbd.calibrate_ranks(kind, a.sim_steps, a.variants, ex, dist)
+        calib = hbd.calibrate_ranks(kind, a.sim_steps, max(1, n_total // ws), ex, dist)
         shares = hb.plan_allocation_n(calib, n_total)
     else:
         shares = [n_total]
@@ -547,11 +558,12 @@ def run_ours(a, ws, rank, local):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "variant-steps/s", "n_gpus": ws,
                 "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None,
                 "dtype": "f32 (float-float positions)" if fp32 and a.model != "box" else "f64",
                 "data": "synthetic (seeds 0..N-1 through build_model; no datasets)",
                 "config": {"workload": workload_name(a), "model": a.model,
-                           "variants_per_gpu": a.variants, "global_variants": n_total,
+                           "variants_per_gpu": n_total // ws if a.scaling == "strong" else a.variants,
+                           "global_variants": n_total,
                            "sim_steps": a.sim_steps,
                            "parallelism": f"dp{ws} (independent variants; contiguous slices "
                                           "from plan_allocation_n)",

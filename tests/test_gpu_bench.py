@@ -71,6 +71,9 @@ def test_bench_two_ranks_batch_and_ea():
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
     shares = d["config"]["splitter"]["shares"]
     assert sum(shares) == 8192 and len(shares) == 2
+    st = _bench_ranks(2, 29533, "--variants", "8192", "--sim-steps", "100", "--steps", "3", "--warmup", "3",
+                      "--no-cpu-baseline", "--scaling", "strong")
+    assert st["scaling"] == "strong" and sum(st["config"]["splitter"]["shares"]) == 8192
     e = _bench_ranks(2, 29532, "--workload", "ea", "--population", "4096", "--generations", "2",
                      "--sim-steps", "100", "--steps", "3", "--warmup", "3")
     assert e["n_gpus"] == 2 and e["value"] > 0
