@@ -51,7 +51,15 @@ def test_bench_ea_line():
     assert d["value"] > 0 and d["host_overhead_us_per_generation"] >= 0
 
 
-def _bench_ranks(nproc, port, *args):
+def _free_port():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _bench_ranks(nproc, _label, *args):
+    port = _free_port()  # the fixed numbers below are only labels
     env = dict(os.environ, HB_DIST_BACKEND="gloo")  # several ranks on one GPU: gloo, not NCCL
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", str(nproc), *args]
