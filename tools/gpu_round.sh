@@ -31,3 +31,8 @@ for f in gpurun_out/*.ncu-rep; do
 done
 cat gpurun_out/saturated.txt
 du -sh gpurun_out
+# the paper's sweeps through the reference's own harness (tools/ref_sweep.cpp)
+mkdir -p gpurun_out/ref_sweep
+timeout 1500 oracle/_ref/ref_sweep tools/sweeps/b200_step_sweep.toml gpurun_out/ref_sweep/step_sweep > gpurun_out/ref_sweep/step_sweep.log 2>&1
+timeout 2400 oracle/_ref/ref_sweep tools/sweeps/b200_variant_grid.toml gpurun_out/ref_sweep/variant_grid > gpurun_out/ref_sweep/variant_grid.log 2>&1
+for f in gpurun_out/ref_sweep/*.log; do tail -n 2 $f; done
