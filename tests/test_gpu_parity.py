@@ -296,6 +296,20 @@ def test_optimised_equals_generic_kernel(gpu, gpu_generic, kind, n, steps):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("kind,n", [(4, 12288), (4, 12289), (1, 65535), (1, 65536), (2, 65535), (2, 65536),
+                                    (4, 65536), (3, 16385)])
+def test_dispatch_boundaries_equal_generic(gpu, gpu_generic, kind, n):
+    """Both sides of every kernel-selection threshold (two-lane CpgHinge up to
+    12 288; register-capped shapes from 65 536; ragged CTAs) against the
+    reference-order generic kernel, every record (tools/parity_fuzz.py is
+    the wider sweep)."""
+    rng = np.random.default_rng(n + 7 * kind)
+    seeds = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64, endpoint=True)
+    a = gpu.run(hb.BatchRequest(kind, seeds, 40)).results
+    b = gpu_generic.run(hb.BatchRequest(kind, seeds, 40)).results
+    assert np.array_equal(a, b)
+
+
 def test_fast_math_replicas(gpu):
     """Branch-free sqrt / div replicas are bit-identical to the library
     wherever they claim validity; out-of-range operands are flagged."""
